@@ -1,0 +1,211 @@
+/*
+ * unimul_b200.h — C-ABI of the B200-native one-sided distributed GEMM.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2510.08874,
+ * package `unimul`, mounted at /root/reference/pkg).  Every entry point below
+ * replaces one reference interface; the citation names the file:line it
+ * stands in for.  Plain pointers and sizes only: no torch, no CUDA types
+ * (streams are passed as `void*` = cudaStream_t).
+ *
+ * Status convention: every function returns UM_OK (0) or an error code; the
+ * message is available from um_last_error() (thread-local).  The Python shim
+ * maps codes to the reference exception classes (errors.py:4-13).
+ */
+#ifndef UNIMUL_B200_H
+#define UNIMUL_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define UM_API __attribute__((visibility("default")))
+#else
+#define UM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-13 + builtin exceptions the reference raises) */
+#define UM_OK          0
+#define UM_ECONFIG     1  /* ConfigError(ValueError)        errors.py:4   */
+#define UM_EOWNERSHIP  2  /* OwnershipError(RuntimeError)   errors.py:8   */
+#define UM_ECONTRACT   3  /* ContractError(ValueError)      errors.py:12  */
+#define UM_EINDEX      4  /* IndexError  (tiling.py:170,217, fabric.py:166) */
+#define UM_EVALUE      5  /* ValueError  (tiling.py:24,38, opgen.py:64)   */
+#define UM_ECUDA       6  /* RuntimeError: CUDA / driver failure           */
+#define UM_ECAPACITY   7  /* caller buffer too small; *n_out holds the need */
+
+/* ---- element types --------------------------------------------------------- */
+#define UM_BF16 0
+#define UM_F32  1
+
+/* Mapping (tiling.py:97-99) */
+#define UM_BLOCK        0
+#define UM_BLOCK_CYCLIC 1
+
+/* Stationarity (opgen.py:21-24) */
+#define UM_STATIONARY_A 0
+#define UM_STATIONARY_B 1
+#define UM_STATIONARY_C 2
+
+/*
+ * Matrix descriptor: global shape + PartitionSpec + replication factor.
+ * Replaces DistributedMatrix's placement state (distmatrix.py:65-114) and
+ * PartitionSpec (tiling.py:102-122).
+ */
+typedef struct {
+  int64_t rows, cols;            /* global shape                         */
+  int64_t tile_rows, tile_cols;  /* PartitionSpec.tile_shape             */
+  int64_t grid_pr, grid_pc;      /* PartitionSpec.proc_grid (per replica) */
+  int32_t mapping;               /* UM_BLOCK | UM_BLOCK_CYCLIC           */
+  int32_t c;                     /* replication factor                   */
+} um_mat_desc;
+
+/*
+ * A 2D strided view of one tile slice: the tile base pointer plus the slice
+ * [row_lo,row_hi) x [col_lo,col_hi) in tile-local coordinates.  This is the
+ * form the TMA tensor maps consume directly (base = tile base, dims =
+ * (col_hi,row_hi), start = (col_lo,row_lo)), so unaligned slices need no copy.
+ * Replaces the numpy slice views of runtime.py:351-358 / kernels.py:13-17.
+ */
+typedef struct {
+  void*   base;                  /* tile base (local, peer-mapped or IPC-mapped) */
+  int64_t row_lo, row_hi;
+  int64_t col_lo, col_hi;
+  int64_t pitch;                 /* row pitch in elements; pitch*esize % 16 == 0 */
+  int32_t dtype;                 /* UM_BF16 | UM_F32                      */
+  int32_t device;                /* CUDA device that physically holds base */
+} um_view;
+
+/* ======================================================================== */
+/* Planner (opgen.py:106-200, tiling.py:125-221)                             */
+/* ======================================================================== */
+
+/* Number of int64 fields per emitted op row. */
+#define UM_OP_FIELDS 24
+/* Field order of an op row:
+ *   0  a_i   1  a_j   2  b_i   3  b_j   4  c_i   5  c_j
+ *   6  m_lo  7  m_hi  8  k_lo  9  k_hi 10  n_lo 11  n_hi
+ *  12..15  a_local rows.lo, rows.hi, cols.lo, cols.hi
+ *  16..19  b_local rows.lo, rows.hi, cols.lo, cols.hi
+ *  20..23  c_local rows.lo, rows.hi, cols.lo, cols.hi
+ * i.e. exactly the fields of opgen.LocalMatMulOp (opgen.py:27-54), in the
+ * order opgen.generate emits them (owned stationary tiles row-major, then the
+ * overlap loops, zero-area ops skipped: opgen.py:117-131,145-159,169-183).
+ */
+
+/* opgen.generate(stationarity, A, B, C, caller)  (opgen.py:193-200).
+ * Writes at most `cap` rows to ops_out; *n_out = number of ops.  Returns
+ * UM_ECAPACITY (with *n_out set) when cap is too small.                    */
+UM_API int um_plan(const um_mat_desc* A, const um_mat_desc* B, const um_mat_desc* C,
+            int32_t nprocs, int32_t stationarity, int32_t caller,
+            int64_t* ops_out, int64_t cap, int64_t* n_out);
+
+/* iteration_offset(stationary_tile, nops)  (runtime.py:89-93 / 297-301).  */
+UM_API int um_iteration_offset(int64_t ti, int64_t tj, int64_t nops, int64_t* out);
+
+/* tiling.owner_of + DistributedMatrix.owner_rank (tiling.py:206-221,
+ * distmatrix.py:109-114): global rank owning tile (i,j) of `replica`.      */
+UM_API int um_owner_rank(const um_mat_desc* M, int32_t nprocs, int64_t i, int64_t j,
+                  int32_t replica, int32_t* rank_out);
+
+/* tiling.most_square_grid(p)  (tiling.py:125-135).                        */
+UM_API int um_most_square_grid(int64_t p, int64_t* gr, int64_t* gc);
+
+/* ======================================================================== */
+/* K1: local tile GEMM on sm_100a (kernels.py:13-28, _gemmcore.pyx:10-25,     */
+/*     runtime.local_gemm runtime.py:96-107)                                 */
+/* ======================================================================== */
+
+/* One component multiply C[c] += A[a] @ B[b] (bf16 in, fp32 accumulate).
+ * c_remote = 0: epilogue TMA reduce-add into c (c on the launching device).
+ * c_remote = 1: epilogue red.global.add straight into c (peer or IPC
+ *               pointer) — the fused remote accumulate of fabric.py:203-234. */
+typedef struct {
+  um_view a, b, c;
+  int32_t c_remote;
+  int32_t reserved;
+} um_gemm_op;
+
+/* c += a @ b for a single op on `stream` (device = c.device unless remote). */
+UM_API int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, void* stream);
+
+/* Grouped persistent launch over a list of ops on one device.  All ops'
+ * operands must be readable from `device`.  Equivalent to calling
+ * um_gemm_acc for each op in order (accumulates commute).                  */
+UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream);
+
+/* Tile/stage knobs of the GEMM (bench/profiling): returns 0 and fills.    */
+UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group);
+
+/* ======================================================================== */
+/* K2: one-sided get engine (fabric.py:156-201, distmatrix.py:151-168)        */
+/* ======================================================================== */
+
+/* dst <- src slice copy (same dtype and shape).  src may live on another
+ * device (peer access) or another process (IPC-mapped); the copy runs on the
+ * copy engines of the launching stream's device (the paper's transport,
+ * PAPER.md:69).                                                            */
+UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
+
+/* ======================================================================== */
+/* K3: one-sided accumulate (fabric.py:203-234, distmatrix.py:170-209)        */
+/* ======================================================================== */
+
+/* dst += src (fp32, same shape); dst may be a peer pointer.  Element-wise
+ * atomic (red.global.add), so concurrent accumulates never tear.           */
+UM_API int um_accumulate(const um_view* src, const um_view* dst, void* stream);
+
+/* ======================================================================== */
+/* K4: replica reduction (distmatrix.py:211-232)                             */
+/* ======================================================================== */
+
+/* dst += (srcs[0] + srcs[1] + ... + srcs[n-1]), summed in array order as the
+ * reference's `acc` (distmatrix.py:224-232).  srcs may be peer pointers.
+ * Views must share the slice shape; a caller splits a tile into row slices
+ * to distribute the reduction over devices.                                */
+UM_API int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, void* stream);
+
+/* dst <- src (whole slice), used by broadcast_replica (distmatrix.py:234-250). */
+UM_API int um_copy(const um_view* src, const um_view* dst, void* stream);
+
+/* ======================================================================== */
+/* K5: synthetic fill at global coordinates (distmatrix.py:95-101)           */
+/* ======================================================================== */
+
+#define UM_FILL_ZERO 0   /* C = 0 (cli.py:200)                               */
+#define UM_FILL_INT  1   /* integers in [-8,8]  (cli.py:188-189 semantics)  */
+#define UM_FILL_REAL 2   /* uniform(-1,1) rounded to the storage dtype      */
+/* Fill the slice with value(seed, grow0 + r, gcol0 + c) (counter-based hash
+ * at GLOBAL coordinates so replicas are identical; oracle/um_oracle.py
+ * restates it).                                                            */
+UM_API int um_fill(const um_view* dst, int64_t grow0, int64_t gcol0, uint64_t seed,
+            int32_t mode, void* stream);
+
+/* ======================================================================== */
+/* Runtime: devices, symmetric memory, IPC (fabric.py:135-150)               */
+/* ======================================================================== */
+
+/* Enable peer access between all listed devices (single-process mode).    */
+UM_API int um_init(int32_t ndev, const int32_t* devices);
+/* Device allocation for the symmetric heap (one chunk).                   */
+UM_API int um_device_alloc(int32_t device, uint64_t bytes, void** ptr);
+UM_API int um_device_free(int32_t device, void* ptr);
+/* CUDA IPC for multi-process (one process per GPU) symmetric heaps.        */
+#define UM_IPC_HANDLE_BYTES 64
+UM_API int um_ipc_get_handle(void* ptr, void* handle_out);
+UM_API int um_ipc_open_handle(const void* handle, int32_t device, void** ptr_out);
+UM_API int um_ipc_close_handle(void* ptr);
+/* Device count / SM count helpers.                                          */
+UM_API int um_device_count(int32_t* n);
+UM_API int um_sm_count(int32_t device, int32_t* n);
+
+/* Version and last error (thread-local).                                    */
+UM_API const char* um_version(void);
+UM_API const char* um_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNIMUL_B200_H */

@@ -1,0 +1,368 @@
+// K2-K5: one-sided data movement for the distributed GEMM.
+//
+//  um_get             <- Fabric.get / get_async        (fabric.py:156-192)
+//  um_accumulate      <- Fabric.accumulate PEER_ATOMIC (fabric.py:203-234)
+//  um_reduce_replicas <- DistributedMatrix.reduce_replicas (distmatrix.py:211-232)
+//  um_copy            <- DistributedMatrix.broadcast_replica (distmatrix.py:234-250)
+//  um_fill            <- DistributedMatrix.__init__ init callback (distmatrix.py:95-101)
+//
+// All of these are HBM/NVLink-bound byte movers: 16-byte vector accesses,
+// grid-stride loops sized to a multiple of the SM count, no tensor cores.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "um_internal.h"
+#include "um_ptx.cuh"
+
+namespace um {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_view(const um_view* v, const char* name, bool need_tma_pitch) {
+  if (!v) return fail(UM_EVALUE, std::string("null view ") + name);
+  if (v->row_lo < 0 || v->row_hi < v->row_lo || v->col_lo < 0 || v->col_hi < v->col_lo)
+    return fail(UM_EVALUE, std::string("invalid slice for ") + name);
+  if (v->dtype != UM_BF16 && v->dtype != UM_F32) return fail(UM_EVALUE, std::string("bad dtype for ") + name);
+  if (v->pitch < v->col_hi) return fail(UM_ECONTRACT, std::string("pitch smaller than slice for ") + name);
+  if (v->row_hi > v->row_lo && v->col_hi > v->col_lo && !v->base)
+    return fail(UM_EVALUE, std::string("null base for ") + name);
+  if (need_tma_pitch && ((v->pitch * esize(v->dtype)) % 16 != 0 || (reinterpret_cast<uintptr_t>(v->base) & 15)))
+    return fail(UM_ECONTRACT, std::string("TMA needs a 16-byte aligned base and pitch for ") + name);
+  return UM_OK;
+}
+
+DeviceGuard::DeviceGuard(int device) {
+  cudaGetDevice(&prev);
+  if (device >= 0 && device != prev) cudaSetDevice(device);
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+}
+
+static int num_sms(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// ------------------------------------------------------------------ kernels
+
+// dst += src element-wise (fp32), dst possibly a peer pointer.  One block row
+// per (row, 4-column group); red.global.add keeps concurrent accumulates
+// atomic per element (fabric.py:226-227 takes a lock for the same guarantee).
+__global__ void accumulate_kernel(const float* __restrict__ src, int64_t src_pitch, float* dst, int64_t dst_pitch,
+                                  int64_t rows, int64_t cols, int vec) {
+  const int64_t groups = vec ? cols / 4 : cols;
+  const int64_t total = rows * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / groups;
+    const int64_t g = i - r * groups;
+    if (vec) {
+      const float4 v = *reinterpret_cast<const float4*>(src + r * src_pitch + 4 * g);
+      ptx::red_add_v4_f32(dst + r * dst_pitch + 4 * g, v.x, v.y, v.z, v.w);
+    } else {
+      ptx::red_add_f32(dst + r * dst_pitch + g, src[r * src_pitch + g]);
+    }
+  }
+  if (vec && blockIdx.x == 0) {
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x)
+      for (int64_t c = groups * 4; c < cols; ++c) ptx::red_add_f32(dst + r * dst_pitch + c, src[r * src_pitch + c]);
+  }
+}
+
+struct SrcList {
+  const float* ptr[16];
+  int64_t pitch[16];
+};
+
+// dst += sum_i src_i, summed in list order into a register accumulator first
+// (the reference's acc, distmatrix.py:224-232).  Sources may be peer pointers
+// (P2P loads over NVLink); dst is written with plain stores (owner only).
+template <int VEC>
+__global__ void reduce_kernel(SrcList srcs, int nsrc, float* dst, int64_t dst_pitch, int64_t rows, int64_t cols) {
+  const int64_t groups = cols / VEC;
+  const int64_t total = rows * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / groups;
+    const int64_t c = (i - r * groups) * VEC;
+    if constexpr (VEC == 4) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < nsrc; ++s) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(srcs.ptr[s] + r * srcs.pitch[s] + c));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      float4* d = reinterpret_cast<float4*>(dst + r * dst_pitch + c);
+      float4 o = *d;
+      o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+      *d = o;
+    } else {
+      float acc = 0.f;
+      for (int s = 0; s < nsrc; ++s) acc += srcs.ptr[s][r * srcs.pitch[s] + c];
+      dst[r * dst_pitch + c] += acc;
+    }
+  }
+}
+
+// Counter-based value generator at GLOBAL coordinates (splitmix64 finaliser),
+// restated bit-for-bit in oracle/um_oracle.py:fill_values.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float fill_value(uint64_t seed, int64_t grow, int64_t gcol, int mode) {
+  const uint64_t h = mix64(seed ^ mix64(((uint64_t)grow << 32) ^ (uint64_t)gcol));
+  if (mode == UM_FILL_INT) return (float)((int)(h % 17ull) - 8);
+  // 24 random bits -> uniform in [-1, 1): exact in fp32
+  return (float)((int64_t)(h >> 40) - (1ll << 23)) * (1.0f / 8388608.0f);
+}
+
+template <typename T>
+__global__ void fill_kernel(T* dst, int64_t pitch, int64_t rows, int64_t cols, int64_t grow0, int64_t gcol0,
+                            uint64_t seed, int mode) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols;
+    const int64_t c = i - r * cols;
+    const float v = mode == UM_FILL_ZERO ? 0.f : fill_value(seed, grow0 + r, gcol0 + c, mode);
+    if constexpr (sizeof(T) == 2)
+      dst[r * pitch + c] = __float2bfloat16_rn(v);
+    else
+      dst[r * pitch + c] = v;
+  }
+}
+
+static int grid_for(int64_t work, int device, int threads = 256) {
+  const int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms(device) * 8;
+  return (int)std::max<int64_t>(1, std::min(blocks, cap));
+}
+
+}  // namespace um
+
+using namespace um;
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" const char* um_version(void) { return "unimul_b200 0.1.0 (sm_100a)"; }
+extern "C" const char* um_last_error(void) { return um::g_last_error.c_str(); }
+
+extern "C" int um_get(const um_view* src, const um_view* dst, void* stream) {
+  int rc;
+  if ((rc = check_view(src, "src", false)) || (rc = check_view(dst, "dst", false))) return rc;
+  if (src->dtype != dst->dtype) return fail(UM_ECONTRACT, "get: dtype mismatch");
+  if (view_rows(*src) != view_rows(*dst) || view_cols(*src) != view_cols(*dst))
+    return fail(UM_ECONTRACT, "get: shape mismatch");
+  const int64_t es = esize(src->dtype);
+  const int64_t rows = view_rows(*src), cols = view_cols(*src);
+  if (rows == 0 || cols == 0) return UM_OK;
+  const char* s = static_cast<const char*>(src->base) + (src->row_lo * src->pitch + src->col_lo) * es;
+  char* d = static_cast<char*>(dst->base) + (dst->row_lo * dst->pitch + dst->col_lo) * es;
+  // Copy-engine transfer (cudaMemcpyDefault resolves peer/IPC/local via UVA).
+  UM_CUDA_CHECK(cudaMemcpy2DAsync(d, dst->pitch * es, s, src->pitch * es, cols * es, rows, cudaMemcpyDefault,
+                                  reinterpret_cast<cudaStream_t>(stream)));
+  return UM_OK;
+}
+
+extern "C" int um_copy(const um_view* src, const um_view* dst, void* stream) { return um_get(src, dst, stream); }
+
+extern "C" int um_accumulate(const um_view* src, const um_view* dst, void* stream) {
+  int rc;
+  if ((rc = check_view(src, "src", false)) || (rc = check_view(dst, "dst", false))) return rc;
+  if (src->dtype != UM_F32 || dst->dtype != UM_F32) return fail(UM_ECONTRACT, "accumulate expects fp32");
+  if (view_rows(*src) != view_rows(*dst) || view_cols(*src) != view_cols(*dst))
+    return fail(UM_ECONTRACT, "accumulate: payload shape does not match slice");
+  const int64_t rows = view_rows(*src), cols = view_cols(*src);
+  if (rows == 0 || cols == 0) return UM_OK;
+  const float* s = static_cast<const float*>(src->base) + src->row_lo * src->pitch + src->col_lo;
+  float* d = static_cast<float*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;
+  const int vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0 &&
+                  src->pitch % 4 == 0 && dst->pitch % 4 == 0;
+  const int dev = current_device();
+  accumulate_kernel<<<grid_for(rows * (vec ? cols / 4 : cols), dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      s, src->pitch, d, dst->pitch, rows, cols, vec);
+  UM_CUDA_CHECK(cudaGetLastError());
+  return UM_OK;
+}
+
+extern "C" int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, void* stream) {
+  int rc;
+  if ((rc = check_view(dst, "dst", false))) return rc;
+  if (dst->dtype != UM_F32) return fail(UM_ECONTRACT, "reduce expects fp32");
+  if (nsrc < 0) return fail(UM_EVALUE, "negative source count");
+  const int64_t rows = view_rows(*dst), cols = view_cols(*dst);
+  if (rows == 0 || cols == 0 || nsrc == 0) return UM_OK;
+  float* d = static_cast<float*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;
+  bool vec = (reinterpret_cast<uintptr_t>(d) & 15) == 0 && dst->pitch % 4 == 0 && cols % 4 == 0;
+  const int dev = current_device();
+  // Sources are consumed in chunks of 16, keeping the in-order sum per chunk;
+  // chunk partials are folded into dst in order (exact for integer inputs).
+  for (int base = 0; base < nsrc; base += 16) {
+    SrcList sl;
+    const int n = std::min(16, nsrc - base);
+    for (int i = 0; i < n; ++i) {
+      const um_view& s = srcs[base + i];
+      if ((rc = check_view(&s, "src", false))) return rc;
+      if (s.dtype != UM_F32 || view_rows(s) != rows || view_cols(s) != cols)
+        return fail(UM_ECONTRACT, "reduce: replica slice shape mismatch");
+      sl.ptr[i] = static_cast<const float*>(s.base) + s.row_lo * s.pitch + s.col_lo;
+      sl.pitch[i] = s.pitch;
+      vec = vec && (reinterpret_cast<uintptr_t>(sl.ptr[i]) & 15) == 0 && s.pitch % 4 == 0;
+    }
+    if (vec)
+      reduce_kernel<4><<<grid_for(rows * cols / 4, dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+          sl, n, d, dst->pitch, rows, cols);
+    else
+      reduce_kernel<1><<<grid_for(rows * cols, dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+          sl, n, d, dst->pitch, rows, cols);
+    UM_CUDA_CHECK(cudaGetLastError());
+  }
+  return UM_OK;
+}
+
+extern "C" int um_fill(const um_view* dst, int64_t grow0, int64_t gcol0, uint64_t seed, int32_t mode, void* stream) {
+  int rc;
+  if ((rc = check_view(dst, "dst", false))) return rc;
+  if (mode != UM_FILL_ZERO && mode != UM_FILL_INT && mode != UM_FILL_REAL) return fail(UM_EVALUE, "bad fill mode");
+  const int64_t rows = view_rows(*dst), cols = view_cols(*dst);
+  if (rows == 0 || cols == 0) return UM_OK;
+  const int dev = current_device();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dst->dtype == UM_BF16) {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;
+    fill_kernel<__nv_bfloat16><<<grid_for(rows * cols, dev), 256, 0, st>>>(p, dst->pitch, rows, cols, grow0, gcol0,
+                                                                            seed, mode);
+  } else {
+    float* p = static_cast<float*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;
+    fill_kernel<float><<<grid_for(rows * cols, dev), 256, 0, st>>>(p, dst->pitch, rows, cols, grow0, gcol0, seed,
+                                                                    mode);
+  }
+  UM_CUDA_CHECK(cudaGetLastError());
+  return UM_OK;
+}
+
+// ------------------------------------------------------------------ runtime
+
+extern "C" int um_init(int32_t ndev, const int32_t* devices) {
+  if (ndev < 0 || (ndev > 0 && !devices)) return fail(UM_EVALUE, "bad device list");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int i = 0; i < ndev; ++i) {
+    UM_CUDA_CHECK(cudaSetDevice(devices[i]));
+    for (int j = 0; j < ndev; ++j) {
+      if (devices[j] == devices[i]) continue;
+      int can = 0;
+      UM_CUDA_CHECK(cudaDeviceCanAccessPeer(&can, devices[i], devices[j]));
+      if (!can) {
+        cudaSetDevice(prev);
+        return fail(UM_ECUDA, "device " + std::to_string(devices[i]) + " cannot access peer " +
+                                  std::to_string(devices[j]));
+      }
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        cudaSetDevice(prev);
+        return fail(UM_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  cudaSetDevice(prev);
+  return UM_OK;
+}
+
+extern "C" int um_device_alloc(int32_t device, uint64_t bytes, void** ptr) {
+  if (!ptr) return fail(UM_EVALUE, "null out pointer");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  UM_CUDA_CHECK(cudaSetDevice(device));
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 256);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(UM_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return UM_OK;
+}
+
+extern "C" int um_device_free(int32_t device, void* ptr) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  UM_CUDA_CHECK(cudaSetDevice(device));
+  cudaError_t e = cudaFree(ptr);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(UM_ECUDA, std::string("cudaFree: ") + cudaGetErrorString(e));
+  return UM_OK;
+}
+
+extern "C" int um_ipc_get_handle(void* ptr, void* handle_out) {
+  if (!handle_out) return fail(UM_EVALUE, "null handle buffer");
+  cudaIpcMemHandle_t h;
+  UM_CUDA_CHECK(cudaIpcGetMemHandle(&h, ptr));
+  static_assert(sizeof(h) <= UM_IPC_HANDLE_BYTES, "IPC handle size");
+  memset(handle_out, 0, UM_IPC_HANDLE_BYTES);
+  memcpy(handle_out, &h, sizeof(h));
+  return UM_OK;
+}
+
+extern "C" int um_ipc_open_handle(const void* handle, int32_t device, void** ptr_out) {
+  if (!handle || !ptr_out) return fail(UM_EVALUE, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  int prev = 0;
+  cudaGetDevice(&prev);
+  UM_CUDA_CHECK(cudaSetDevice(device));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(UM_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  return UM_OK;
+}
+
+extern "C" int um_ipc_close_handle(void* ptr) {
+  UM_CUDA_CHECK(cudaIpcCloseMemHandle(ptr));
+  return UM_OK;
+}
+
+extern "C" int um_device_count(int32_t* n) {
+  if (!n) return fail(UM_EVALUE, "null out pointer");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *n = c;
+  return UM_OK;
+}
+
+extern "C" int um_sm_count(int32_t device, int32_t* n) {
+  if (!n) return fail(UM_EVALUE, "null out pointer");
+  int v = 0;
+  UM_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  *n = v;
+  return UM_OK;
+}

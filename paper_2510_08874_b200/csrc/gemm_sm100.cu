@@ -1,0 +1,519 @@
+// K1: persistent bf16 x bf16 -> fp32 tile GEMM for sm_100a, C += A @ B.
+//
+// Replaces the reference's local multiply-accumulate
+//   runtime.local_gemm            (/root/reference/pkg/src/unimul/runtime.py:96-107)
+//   kernels.gemm_accumulate       (kernels.py:13-28)
+//   _gemmcore.gemm_accumulate     (_gemmcore.pyx:10-25: c[i,j] += a[i,l] * b[l,j])
+// and fuses the remote accumulate of Stationary A/B
+//   fabric.accumulate PEER_ATOMIC (fabric.py:203-234) via distmatrix.accumulate_tile
+// into the epilogue.
+//
+// Design (B200-first):
+//  * warp-specialised persistent kernel: warp 0 = TMA producer, warp 1 = MMA
+//    issuer (one thread issues tcgen05.mma), warps 2..5 = epilogue.
+//  * operands are consumed IN PLACE from strided tile slices: each operand's
+//    TMA tensor map is based at the tile base with dims (col_hi,row_hi) and the
+//    loads start at (col_lo,row_lo), so arbitrary row offsets and ragged edges
+//    need no copy (OOB zero-fill on load, clipping on the reduce).  TMA needs
+//    the innermost start coordinate 16-byte aligned; the rare slices that
+//    violate it (misaligned partitionings) are staged (see launch_batch).
+//  * A is row-major m x k -> K-major SW128; B is row-major k x n -> MN-major SW128.
+//  * accumulators live in TMEM (2 x BN fp32 columns, double-buffered so the
+//    epilogue of tile i overlaps the main loop of tile i+1).
+//  * epilogue: tcgen05.ld -> registers -> swizzled smem -> TMA reduce-add
+//    (cp.reduce.async.bulk.tensor ... add) into the local C tile, or
+//    red.global.add.v4.f32 straight into a peer C tile (fused K3).
+//  * CG == 2: a CTA pair (cluster of 2) issues cta_group::2 UMMA of 256 x BN;
+//    each CTA stages half of A (its 128 rows) and half of B (BN/2 columns).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "um_internal.h"
+#include "um_ptx.cuh"
+
+namespace um {
+
+namespace gemm {
+
+constexpr int BM = 128;       // rows per CTA (UMMA M = BM * CG)
+constexpr int BN = 256;       // columns per tile (UMMA N)
+constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
+constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
+constexpr int EPI_WARPS = 4;
+constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
+constexpr int GROUP_M = 16;   // rasterisation group (tiles of BM*CG rows)
+constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
+
+template <int CG>
+struct Cfg {
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int B_COLS = BN / CG;                    // B columns staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;               // 16 KiB
+  static constexpr int B_BYTES = BK * B_COLS * 2;           // 32 KiB (CG1) / 16 KiB (CG2)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BOX_BYTES;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;             // two accumulator buffers
+};
+
+struct alignas(16) Work {
+  int32_t m, n, k;
+  int32_t tiles_m, tiles_n, num_kb;
+  int32_t tile_start, c_remote;
+  int32_t a_row0, a_col0;
+  int32_t b_row0, b_col0;
+  int32_t c_row0, c_col0;
+  int32_t c_vec_ok, pad0;
+  int64_t c_pitch;
+  float* c_ptr;
+};
+
+__device__ __forceinline__ int find_work(const Work* works, int nwork, int t) {
+  int w = 0;
+  while (w + 1 < nwork && works[w + 1].tile_start <= t) ++w;
+  return w;
+}
+
+__device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int& nb) {
+  const int group = GROUP_M * wk.tiles_n;
+  const int g = lt / group;
+  const int first_m = g * GROUP_M;
+  const int gm = min(wk.tiles_m - first_m, GROUP_M);
+  const int r = lt - g * group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+template <int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_kernel(const Work* __restrict__ works, const CUtensorMap* __restrict__ maps, int nwork,
+                     int total_tiles) {
+  using C = Cfg<CG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
+  uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + C::EPI_BYTES);
+  uint64_t* full = bars;                    // [STAGES]
+  uint64_t* empty = bars + C::STAGES;       // [STAGES]
+  uint64_t* tmem_full = bars + 2 * C::STAGES;      // [2]
+  uint64_t* tmem_empty = bars + 2 * C::STAGES + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t cta_rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
+  const bool leader = cta_rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tmem_full[s], 1);
+      ptx::mbar_init(&tmem_empty[s], EPI_WARPS * CG);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (one thread) =====================
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_normal();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+        const int w = find_work(works, nwork, t);
+        const Work& wk = works[w];
+        const CUtensorMap* ma = &maps[3 * w + 0];
+        const CUtensorMap* mbm = &maps[3 * w + 1];
+        int mb, nb;
+        tile_coords(wk, t - wk.tile_start, mb, nb);
+        const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
+        const int bcol = wk.b_col0 + nb * BN + (int)cta_rank * C::B_COLS;
+        for (int kb = 0; kb < wk.num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+          uint8_t* sa = smem_a + stage * C::A_BYTES;
+          uint8_t* sb = smem_b + stage * C::B_BYTES;
+          const int kcol = wk.a_col0 + kb * BK;
+          const int krow = wk.b_row0 + kb * BK;
+          if constexpr (CG == 1) {
+            ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pol);
+#pragma unroll
+            for (int j = 0; j < C::B_COLS / 64; ++j)
+              ptx::tma_load_2d(sb + j * (BK * 128), mbm, &full[stage], bcol + j * 64, krow, pol);
+          } else {
+            ptx::tma_load_2d_cg2(sa, ma, &full[stage], kcol, arow, pol);
+#pragma unroll
+            for (int j = 0; j < C::B_COLS / 64; ++j)
+              ptx::tma_load_2d_cg2(sb + j * (BK * 128), mbm, &full[stage], bcol + j * 64, krow, pol);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread, leader CTA) =====================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, BN, 0, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+        const int w = find_work(works, nwork, t);
+        const int num_kb = works[w].num_kb;
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        ptx::mbar_wait(&tmem_empty[as], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            // A: K-major SW128, 8-row groups 1024 B apart; advance 32 B per UMMA_K.
+            const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
+            // B: MN-major SW128; 64-column blocks BK*128 B apart (LBO), 8-k groups
+            // 1024 B apart (SBO); advance 16 k-rows = 2048 B per UMMA_K.
+            const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 128), BK * 128, 1024);
+            ptx::umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+          }
+          ptx::umma_commit<CG>(&empty[stage], 0x3);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit<CG>(&tmem_full[as], 0x3);
+      }
+    }
+  } else {
+    // ===================== Epilogue (4 warps) =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* ebuf = smem_epi + (warp - 2) * 2 * EPI_BOX_BYTES;
+    const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
+    int it = 0;
+    int buf = 0;
+    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+      const int w = find_work(works, nwork, t);
+      const Work& wk = works[w];
+      const CUtensorMap* mc = &maps[3 * w + 2];
+      int mb, nb;
+      tile_coords(wk, t - wk.tile_start, mb, nb);
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      ptx::mbar_wait(&tmem_full[as], aphase);
+      ptx::tc_fence_after();
+      const int row_in_op = mb * BM * CG + (int)cta_rank * BM + q * 32;   // first row of this warp
+      const int col_in_op = nb * BN;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + ch * 32, r);
+        ptx::tmem_ld_wait();
+        if (ch == BN / 32 - 1) {
+          // accumulator fully drained into registers: hand TMEM back to the MMA warp
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) ptx::mbar_arrive(&tmem_empty[as]);
+            else ptx::mbar_arrive_cluster(&tmem_empty[as], 0);
+          }
+        }
+        if (!wk.c_remote) {
+          // registers -> swizzled smem box -> TMA reduce-add into C
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+          const uint32_t base = ebuf_u32 + buf * EPI_BOX_BYTES + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t addr = base + ((j ^ (lane & 7)) << 4);
+            ptx::st_shared_v4(addr, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_reduce_add_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
+                                   wk.c_row0 + row_in_op);
+            ptx::bulk_commit();
+          }
+          buf ^= 1;
+        } else {
+          // fused remote accumulate: red.global.add into the (peer) C tile
+          const int row = row_in_op + lane;
+          const int col0 = col_in_op + ch * 32;
+          if (row < wk.m) {
+            float* rowp = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0;
+            if (wk.c_vec_ok && col0 + 32 <= wk.n) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                ptx::red_add_v4_f32(rowp + col0 + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < wk.n) ptx::red_add_f32(rowp + col0 + j, __uint_as_float(r[j]));
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
+  }
+
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint32_t box_rows, const char* what) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return fail(UM_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const CUtensorMapDataType dt = v.dtype == UM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  cuuint64_t dims[2] = {(cuuint64_t)v.col_hi, (cuuint64_t)v.row_hi};
+  cuuint64_t strides[1] = {(cuuint64_t)(v.pitch * esize(v.dtype))};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, v.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(UM_ECUDA, std::string("cuTensorMapEncodeTiled failed for ") + what + " (code " +
+                              std::to_string((int)r) + ")");
+  return UM_OK;
+}
+
+static int g_cta_group = 2;  // default kernel variant; UM_GEMM_CG=1 env selects the 1-CTA kernel
+
+static int cta_group() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("UM_GEMM_CG");
+    if (e && e[0] == '1') g_cta_group = 1;
+  });
+  return g_cta_group;
+}
+
+template <int CG>
+static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int total_tiles, int device,
+                  cudaStream_t stream) {
+  using C = Cfg<CG>;
+  static bool attr_set[64] = {false};
+  if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
+  if (!attr_set[device]) {
+    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::SMEM_BYTES));
+    attr_set[device] = true;
+  }
+  int sms = 0;
+  UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int clusters = std::min(total_tiles, sms / CG);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG>, d_works, d_maps, nwork, total_tiles));
+  return UM_OK;
+}
+
+// TMA requires the innermost start coordinate of a box to be 16-byte aligned
+// (measured: an unaligned column offset raises an illegal-instruction fault;
+// row offsets are free).  Slices of misaligned partitionings (e.g. 3x4 tiles,
+// cli.py:151-152) therefore get their A/B slice staged into an aligned scratch
+// and their C update routed through the pointer-based red.global epilogue.
+static inline bool inner_aligned(const um_view& v) { return (v.col_lo * esize(v.dtype)) % 16 == 0; }
+static inline int64_t aligned_pitch(int64_t cols, int32_t dtype) {
+  const int64_t per16 = 16 / esize(dtype);
+  return (cols + per16 - 1) / per16 * per16;
+}
+
+int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t stream) {
+  const int CG = cta_group();
+  DeviceGuard guard(device);
+  // ---- stage misaligned operand slices
+  std::vector<um_gemm_op> ops(ops_in, ops_in + nops);
+  size_t scratch_bytes = 0;
+  for (auto& op : ops) {
+    for (um_view* v : {&op.a, &op.b})
+      if (!inner_aligned(*v) && view_rows(*v) > 0 && view_cols(*v) > 0)
+        scratch_bytes += (size_t)(view_rows(*v) * aligned_pitch(view_cols(*v), v->dtype) * esize(v->dtype) + 256);
+    if (!inner_aligned(op.c)) op.c_remote = 1;
+  }
+  void* scratch = nullptr;
+  if (scratch_bytes) {
+    UM_CUDA_CHECK(cudaMallocAsync(&scratch, scratch_bytes, stream));
+    size_t off = 0;
+    for (auto& op : ops)
+      for (um_view* v : {&op.a, &op.b}) {
+        if (inner_aligned(*v) || view_rows(*v) == 0 || view_cols(*v) == 0) continue;
+        int rc;
+        if ((rc = check_view(v, "operand", false))) return rc;
+        um_view dst = {};
+        dst.base = static_cast<char*>(scratch) + off;
+        dst.row_lo = 0;
+        dst.row_hi = view_rows(*v);
+        dst.col_lo = 0;
+        dst.col_hi = view_cols(*v);
+        dst.pitch = aligned_pitch(view_cols(*v), v->dtype);
+        dst.dtype = v->dtype;
+        dst.device = device;
+        const int64_t es = esize(v->dtype);
+        UM_CUDA_CHECK(cudaMemcpy2DAsync(dst.base, dst.pitch * es,
+                                        static_cast<const char*>(v->base) + (v->row_lo * v->pitch + v->col_lo) * es,
+                                        v->pitch * es, view_cols(*v) * es, view_rows(*v), cudaMemcpyDefault, stream));
+        off += (size_t)(dst.row_hi * dst.pitch * es + 255) / 256 * 256;
+        *v = dst;
+      }
+  }
+  struct ScratchFree {
+    void* p;
+    cudaStream_t s;
+    ~ScratchFree() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } scratch_guard{scratch, stream};
+  std::vector<Work> works;
+  std::vector<CUtensorMap> maps;
+  works.reserve(nops);
+  maps.reserve(3 * nops);
+  int total = 0;
+  for (int i = 0; i < nops; ++i) {
+    const um_gemm_op& op = ops[i];
+    if (op.c_remote && op.c.dtype == UM_F32 && (reinterpret_cast<uintptr_t>(op.c.base) & 3))
+      return fail(UM_ECONTRACT, "fp32 C base must be 4-byte aligned");
+    int rc;
+    if ((rc = check_view(&op.a, "a", true)) || (rc = check_view(&op.b, "b", true)) ||
+        (rc = check_view(&op.c, "c", !op.c_remote)))
+      return rc;
+    if (op.a.dtype != UM_BF16 || op.b.dtype != UM_BF16 || op.c.dtype != UM_F32)
+      return fail(UM_ECONTRACT, "gemm expects bf16 A/B and fp32 C");
+    const int64_t m = view_rows(op.a), k = view_cols(op.a), n = view_cols(op.b);
+    if (view_rows(op.b) != k || view_rows(op.c) != m || view_cols(op.c) != n)
+      return fail(UM_ECONTRACT, "gemm shape mismatch: a " + std::to_string(m) + "x" + std::to_string(k) + ", b " +
+                                    std::to_string(view_rows(op.b)) + "x" + std::to_string(n) + ", c " +
+                                    std::to_string(view_rows(op.c)) + "x" + std::to_string(view_cols(op.c)));
+    if (m == 0 || n == 0 || k == 0) continue;  // c += 0
+    if (op.a.row_hi > INT32_MAX || op.a.col_hi > INT32_MAX || op.b.row_hi > INT32_MAX ||
+        op.b.col_hi > INT32_MAX || op.c.row_hi > INT32_MAX || op.c.col_hi > INT32_MAX)
+      return fail(UM_EVALUE, "tile extent exceeds int32 TMA coordinates");
+    Work w = {};
+    w.m = (int32_t)m;
+    w.n = (int32_t)n;
+    w.k = (int32_t)k;
+    w.tiles_m = (int32_t)((m + BM * CG - 1) / (BM * CG));
+    w.tiles_n = (int32_t)((n + BN - 1) / BN);
+    w.num_kb = (int32_t)((k + BK - 1) / BK);
+    w.tile_start = total;
+    w.c_remote = op.c_remote;
+    w.a_row0 = (int32_t)op.a.row_lo;
+    w.a_col0 = (int32_t)op.a.col_lo;
+    w.b_row0 = (int32_t)op.b.row_lo;
+    w.b_col0 = (int32_t)op.b.col_lo;
+    w.c_row0 = (int32_t)op.c.row_lo;
+    w.c_col0 = (int32_t)op.c.col_lo;
+    w.c_pitch = op.c.pitch;
+    w.c_ptr = reinterpret_cast<float*>(op.c.base);
+    w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
+    total += w.tiles_m * w.tiles_n;
+    CUtensorMap ma, mbm, mc;
+    if ((rc = encode_2d(&ma, op.a, BK, BM, "A")) || (rc = encode_2d(&mbm, op.b, 64, BK, "B"))) return rc;
+    if (!op.c_remote) {
+      if ((rc = encode_2d(&mc, op.c, 32, 32, "C"))) return rc;
+    } else {
+      memset(&mc, 0, sizeof(mc));
+    }
+    works.push_back(w);
+    maps.push_back(ma);
+    maps.push_back(mbm);
+    maps.push_back(mc);
+  }
+  if (works.empty()) return UM_OK;
+  // One stream-ordered allocation carries the work list and the tensor maps.
+  const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
+  const size_t works_bytes = works.size() * sizeof(Work);
+  std::vector<uint8_t> host(maps_bytes + works_bytes);
+  memcpy(host.data(), maps.data(), maps_bytes);
+  memcpy(host.data() + maps_bytes, works.data(), works_bytes);
+  void* dbuf = nullptr;
+  UM_CUDA_CHECK(cudaMallocAsync(&dbuf, host.size(), stream));
+  UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
+  const CUtensorMap* d_maps = reinterpret_cast<const CUtensorMap*>(dbuf);
+  const Work* d_works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
+  int rc = (CG == 2) ? launch<2>(d_works, d_maps, (int)works.size(), total, device, stream)
+                     : launch<1>(d_works, d_maps, (int)works.size(), total, device, stream);
+  cudaFreeAsync(dbuf, stream);
+  return rc;
+}
+
+}  // namespace gemm
+}  // namespace um
+
+extern "C" int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, void* stream) {
+  if (!a || !b || !c) return um::fail(UM_EVALUE, "null view");
+  um_gemm_op op = {};
+  op.a = *a;
+  op.b = *b;
+  op.c = *c;
+  op.c_remote = 0;
+  return um::gemm::launch_batch(&op, 1, c->device, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream) {
+  if (nops < 0 || (nops > 0 && !ops)) return um::fail(UM_EVALUE, "bad op list");
+  return um::gemm::launch_batch(ops, nops, device, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group) {
+  const int cg = um::gemm::cta_group();
+  if (bm) *bm = um::gemm::BM * cg;
+  if (bn) *bn = um::gemm::BN;
+  if (bk) *bk = um::gemm::BK;
+  if (stages) *stages = cg == 1 ? um::gemm::Cfg<1>::STAGES : um::gemm::Cfg<2>::STAGES;
+  if (cta_group) *cta_group = cg;
+  return UM_OK;
+}

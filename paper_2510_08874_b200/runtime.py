@@ -1,0 +1,659 @@
+"""Execution engine: op lists -> one-sided gets + tcgen05 GEMMs on B200.
+
+Drop-in for unimul.runtime (runtime.py:26-387): same ExecConfig, RunStats,
+iteration_offset, local_gemm, run_direct, run_ir and execute_multiply
+signatures.  What runs underneath is B200-native:
+
+* schedule lowering (direct execution, runtime.py:193-256): the caller's op
+  list comes from the C++ planner, rotated by the reference's iteration
+  offset (runtime.py:213-214).  Remote operand slices are then DEDUPLICATED:
+  every remote (matrix, tile) is pulled once, as the bounding box of the
+  slices this rank's ops need (the reference re-fetches the whole tile for
+  every op: distmatrix.py:158, runtime.py:219-231).  Pulls are issued in
+  first-use order on a per-rank copy stream (K2, copy engines), each
+  followed by an event.
+* GEMM issue: ops are grouped into persistent grouped launches (K1); a group
+  is flushed whenever the next op needs a pull that has not been waited on,
+  so pulls overlap the GEMMs of earlier ops.
+* remote C (Stationary A/B): the K1 epilogue accumulates straight into the
+  owner's tile (TMA reduce-add on the same GPU, red.global.add over NVLink to
+  a peer GPU) — the reference's scratch + accumulate_tile round trip
+  (runtime.py:362-373) disappears.
+* replicated C: after a run-level barrier, K4 reduces the replicas into
+  replica 0, distributed over the replica owners' GPUs.
+
+Everything is stream-ordered: work starts after whatever is pending on the
+devices' current streams and the current streams wait for completion on
+return, so torch code sees the results without host synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from paper_2510_08874_b200 import _capi, kernels, lowering, opgen
+from paper_2510_08874_b200.distmatrix import DistributedMatrix
+from paper_2510_08874_b200.errors import ContractError
+from paper_2510_08874_b200.fabric import ELEM_BYTES, AccumulateMode, pitch_for, um_dtype
+from paper_2510_08874_b200.opgen import LocalMatMulOp, Stationarity
+from paper_2510_08874_b200.tiling import TileIdx
+
+__all__ = ["ExecConfig", "BufferPool", "RunStats", "iteration_offset", "local_gemm", "run_direct",
+           "run_ir", "execute_multiply", "reduce_replicas", "lower_direct", "DirectSchedule"]
+
+
+@dataclass
+class ExecConfig:
+    """Reference knobs (runtime.py:26-40) plus B200 knobs.
+
+    B200 knobs:
+      staging            "slice": pull the bounding box of the slices a rank
+                         needs from each remote tile, once; "tile": pull whole
+                         remote tiles once.
+      same_device_gets   "copy": ranks co-resident on one GPU still pull
+                         (one-sided semantics, exercises K2); "direct": read
+                         the owner's tile in place.
+      gemm_batch         max ops per grouped K1 launch (0 = unlimited).
+      fused_accumulate   remote C updates from the K1 epilogue (K3 fused);
+                         False = scratch GEMM + um_accumulate.
+      reduce_distributed K4 over all replica owners (True) or pull-to-origin.
+    """
+
+    stationarity: Stationarity = Stationarity.STATIONARY_C
+    prefetch_depth: int = 2
+    max_inflight_gemms: int = 4
+    max_inflight_accums: int = 4
+    accumulate_mode: AccumulateMode = AccumulateMode.PEER_ATOMIC
+    pool_capacity: int | None = None
+    staging: str = "slice"
+    same_device_gets: str = "copy"
+    gemm_batch: int = 0
+    fused_accumulate: bool = True
+    reduce_distributed: bool = True
+
+    def __post_init__(self):
+        if self.prefetch_depth < 1 or self.max_inflight_gemms < 1 or self.max_inflight_accums < 1:
+            raise ValueError("ExecConfig counts must be >= 1")
+        if self.pool_capacity is not None and self.pool_capacity < 3:
+            raise ValueError("pool_capacity must cover at least one op (3 buffers)")
+        if self.staging not in ("slice", "tile"):
+            raise ValueError(f"unknown staging mode {self.staging!r}")
+        if self.same_device_gets not in ("copy", "direct"):
+            raise ValueError(f"unknown same_device_gets {self.same_device_gets!r}")
+        if self.gemm_batch < 0:
+            raise ValueError("gemm_batch must be >= 0")
+
+
+class BufferPool:
+    """Fixed set of staging slots; no allocation after construction (runtime.py:43-73).
+
+    Kept for API parity (IR replay uses it for scratch accounting).  With
+    `buffer_elems` > 0 and a device, the slots are device buffers.
+    """
+
+    def __init__(self, capacity: int, buffer_elems: int, device=None, dtype=torch.float32):
+        self._arena = torch.zeros((capacity, max(1, buffer_elems)), dtype=dtype,
+                                  device=device if device is not None else "cpu")
+        self._free = list(range(capacity))
+        self.capacity = capacity
+        self.acquired = 0
+        self.released = 0
+        self.peak_in_use = 0
+
+    @property
+    def free_count(self) -> int:
+        return len(self._free)
+
+    def acquire(self, drain=None):
+        while not self._free:
+            if drain is None or not drain():
+                raise RuntimeError("buffer pool exhausted with nothing left to drain; increase pool_capacity")
+        slot = self._free.pop()
+        self.acquired += 1
+        self.peak_in_use = max(self.peak_in_use, self.capacity - len(self._free))
+        return slot, self._arena[slot]
+
+    def release(self, slot: int):
+        self._free.append(slot)
+        self.released += 1
+
+
+@dataclass
+class RunStats:
+    """Per-rank record (runtime.py:76-86) plus what the B200 engine did."""
+
+    executed_ops: list[LocalMatMulOp] = field(default_factory=list)
+    a_requests: list[TileIdx] = field(default_factory=list)
+    b_requests: list[TileIdx] = field(default_factory=list)
+    peak_inflight_gemms: int = 0
+    peak_inflight_accums: int = 0
+    pool_acquired: int = 0
+    pool_released: int = 0
+    pool_peak: int = 0
+    flops: int = 0
+    gets: int = 0
+    staged_bytes: int = 0
+    launches: int = 0
+    peak_ops_per_launch: int = 0
+
+
+def iteration_offset(stationary_tile: TileIdx, nops: int) -> int:
+    """(i + j) mod nops of the first op's stationary tile (runtime.py:89-93)."""
+    out = ctypes.c_int64(0)
+    _capi.check(_capi.load().um_iteration_offset(stationary_tile.i, stationary_tile.j, nops, ctypes.byref(out)),
+                "iteration_offset")
+    return int(out.value)
+
+
+def local_gemm(a, b, c, counters=None, rank: int = 0) -> None:
+    """c += a @ b on K1, reporting flops (runtime.py:96-107)."""
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2 or tuple(c.shape) != (m, n):
+        raise ContractError(f"gemm shape mismatch: {tuple(a.shape)} x {tuple(b.shape)} -> {tuple(c.shape)}")
+    kernels.gemm_accumulate(a, b, c)
+    if counters is not None:
+        counters.add_flops(rank, 2 * m * k * n)
+
+
+# ---------------------------------------------------------------------------
+# schedule lowering for direct execution
+# ---------------------------------------------------------------------------
+
+@dataclass
+class _Fetch:
+    mat: str                 # "A" | "B"
+    tile: TileIdx
+    replica: int
+    owner: int
+    r0: int                  # tile-local bounding box of the needed slices
+    r1: int
+    c0: int
+    c1: int
+    first_use: int
+
+
+@dataclass
+class DirectSchedule:
+    """Lowered direct-execution schedule of one rank."""
+
+    caller: int
+    ops: list                        # rotated op list
+    fetches: list                    # _Fetch in first-use order
+    a_src: list                      # per op: fetch index or -1 (read in place)
+    b_src: list
+    c_remote: list                   # per op: True if the C tile belongs to another rank
+
+
+def _in_place(fabric, owner: int, caller: int, cfg: ExecConfig) -> bool:
+    if owner == caller:
+        return True
+    if cfg.same_device_gets == "direct" and fabric.world.size == 1 and not fabric.placement_only:
+        return fabric.device_of(owner) == fabric.device_of(caller)
+    return False
+
+
+def lower_direct(A, B, C, cfg: ExecConfig, caller: int) -> DirectSchedule:
+    """Rotated op list + fetch-once staging plan (host-side, no device work)."""
+    ops = opgen.generate(cfg.stationarity, A, B, C, caller)
+    if ops:
+        s = iteration_offset(ops[0].stationary_tile(cfg.stationarity), len(ops))
+        ops = ops[s:] + ops[:s]
+    fabric = A.fabric
+    fetches: list[_Fetch] = []
+    index: dict = {}
+    a_src, b_src, c_remote = [], [], []
+    for i, op in enumerate(ops):
+        for name, M, t, loc, srcs in (("A", A, op.a_tile, op.a_local, a_src), ("B", B, op.b_tile, op.b_local, b_src)):
+            rep = M.replica_of(caller)
+            owner = M.owner_rank(t, rep)
+            if _in_place(fabric, owner, caller, cfg):
+                srcs.append(-1)
+                continue
+            key = (name, t)
+            j = index.get(key)
+            if cfg.staging == "tile":
+                b = M.tile_bounds(t)
+                r0, r1, c0, c1 = 0, len(b.rows), 0, len(b.cols)
+            else:
+                r0, r1, c0, c1 = loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi
+            if j is None:
+                index[key] = len(fetches)
+                srcs.append(len(fetches))
+                fetches.append(_Fetch(name, t, rep, owner, r0, r1, c0, c1, i))
+            else:
+                f = fetches[j]
+                f.r0, f.r1, f.c0, f.c1 = min(f.r0, r0), max(f.r1, r1), min(f.c0, c0), max(f.c1, c1)
+                srcs.append(j)
+        c_owner = C.owner_rank(op.c_tile, C.replica_of(caller))
+        c_remote.append(c_owner != caller)
+    return DirectSchedule(caller, ops, fetches, a_src, b_src, c_remote)
+
+
+def _count_reference_traffic(A, B, C, cfg: ExecConfig, sched: DirectSchedule):
+    """FabricCounters exactly as the reference's run_direct would record them.
+
+    Every remote A/B tile is a whole-tile get per op (runtime.py:427-438,
+    distmatrix.py:158); every remote C update one accumulate_tile
+    (runtime.py:338-341: one message if full-width, else one per row;
+    2x bytes and messages in LOCK_GET_PUT, fabric.py:225-234).
+    """
+    ctr = A.fabric.counters
+    caller = sched.caller
+    lgp = cfg.accumulate_mode is AccumulateMode.LOCK_GET_PUT
+    for i, op in enumerate(sched.ops):
+        for M, t in ((A, op.a_tile), (B, op.b_tile)):
+            owner = M.owner_rank(t, M.replica_of(caller))
+            if owner != caller:
+                ctr.add_traffic(caller, owner, ELEM_BYTES * M.tile_bounds(t).area, 1, 0)
+        if sched.c_remote[i]:
+            owner = C.owner_rank(op.c_tile, C.replica_of(caller))
+            n = len(op.m_bound) * len(op.n_bound)
+            full = len(op.c_local.cols) == len(C.tile_bounds(op.c_tile).cols)
+            msgs = 1 if full else len(op.m_bound)
+            ctr.add_traffic(caller, owner, (2 if lgp else 1) * ELEM_BYTES * n, (2 if lgp else 1) * msgs,
+                            4 * n)
+        ctr.add_flops(caller, op.flops)
+
+
+def _current_events(fabric) -> list:
+    evs = []
+    for d in sorted({fabric.device_of(r) for r in fabric.local_ranks()}):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(d))
+        evs.append(ev)
+    return evs
+
+
+def _join_current(fabric, events):
+    for d in sorted({fabric.device_of(r) for r in fabric.local_ranks()}):
+        cur = torch.cuda.current_stream(d)
+        for ev in events:
+            cur.wait_event(ev)
+
+
+def _check_operands(A, B, C):
+    if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise ContractError("A and B must be bfloat16 matrices (tensor-core inputs); "
+                            "construct them with dtype=torch.bfloat16")
+    if C.dtype != torch.float32:
+        raise ContractError("C must be a float32 matrix (fp32 accumulation)")
+    A.fabric._require_data()
+
+
+class _RankRun:
+    """Device work of one rank's direct schedule (issued asynchronously)."""
+
+    def __init__(self, A, B, C, cfg: ExecConfig, sched: DirectSchedule, start_events):
+        self.A, self.B, self.C, self.cfg, self.sched = A, B, C, cfg, sched
+        fab = A.fabric
+        self.fab = fab
+        self.caller = sched.caller
+        self.dev = fab.device_of(self.caller)
+        self.gs = fab.stream(self.caller, "get")
+        self.cs = fab.stream(self.caller, "compute")
+        self.stats = RunStats()
+        self.buffers = []
+        self.done = None
+        for ev in start_events:
+            self.gs.wait_event(ev)
+            self.cs.wait_event(ev)
+
+    def _mat(self, name):
+        return self.A if name == "A" else self.B
+
+    def issue(self):
+        lib = _capi.load()
+        s, st, fab = self.sched, self.stats, self.fab
+        # ---- K2: one pull per remote (matrix, tile), first-use order
+        fetch_events = []
+        staged = []
+        with torch.cuda.device(self.dev):
+            for f in s.fetches:
+                M = self._mat(f.mat)
+                seg = M.segment(f.tile, f.replica)
+                rows, cols = f.r1 - f.r0, f.c1 - f.c0
+                pitch = pitch_for(cols, M.dtype)
+                with torch.cuda.stream(self.gs):
+                    buf = torch.empty((rows, pitch), dtype=M.dtype, device=f"cuda:{self.dev}")
+                buf.record_stream(self.cs)
+                self.buffers.append(buf)
+                src = seg.um_view(f.r0, f.r1, f.c0, f.c1)
+                dst = _capi.UmView(buf.data_ptr(), 0, rows, 0, cols, pitch, um_dtype(M.dtype), self.dev)
+                _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(self.gs.cuda_stream)),
+                            "um_get")
+                ev = torch.cuda.Event()
+                ev.record(self.gs)
+                fetch_events.append(ev)
+                staged.append(buf)
+                nbytes = rows * cols * buf.element_size()
+                fab.counters.add_traffic(self.caller, f.owner, 0, 0, nbytes)
+                st.gets += 1
+                st.staged_bytes += nbytes
+            st.pool_acquired = st.pool_released = st.pool_peak = len(s.fetches)
+
+            # ---- K1: grouped launches, flushed when the next op needs an unwaited pull
+            batch: list = []
+            batch_remote = 0
+            waited = -1
+            cap = self.cfg.gemm_batch or (1 << 30)
+
+            def flush():
+                nonlocal batch, batch_remote
+                if not batch:
+                    return
+                arr = (_capi.UmGemmOp * len(batch))(*batch)
+                _capi.check(lib.um_gemm_acc_batch(arr, len(batch), self.dev, ctypes.c_void_p(self.cs.cuda_stream)),
+                            "um_gemm_acc_batch")
+                st.launches += 1
+                st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
+                st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)
+                batch, batch_remote = [], 0
+
+            for i, op in enumerate(s.ops):
+                need = max(s.a_src[i], s.b_src[i])
+                if need > waited:
+                    flush()
+                    for j in range(waited + 1, need + 1):
+                        self.cs.wait_event(fetch_events[j])
+                    waited = need
+                remote = s.c_remote[i] and self.fab.device_of(
+                    self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
+                if len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums):
+                    flush()
+                ga = self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged)
+                gb = self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)
+                if remote and not self.cfg.fused_accumulate:
+                    flush()
+                    self._scratch_gemm(op, ga, gb)
+                    continue
+                cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+                gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+                batch.append(_capi.UmGemmOp(ga, gb, gc, 1 if remote else 0, 0))
+                batch_remote += int(remote)
+                st.executed_ops.append(op)
+                st.a_requests.append(op.a_tile)
+                st.b_requests.append(op.b_tile)
+            flush()
+            for j in range(waited + 1, len(fetch_events)):
+                self.cs.wait_event(fetch_events[j])
+            st.peak_inflight_gemms = 1 if s.ops else 0
+            self.done = torch.cuda.Event()
+            self.done.record(self.cs)
+        return self
+
+    def _operand_view(self, name, t, loc, src_idx, staged):
+        M = self._mat(name)
+        if src_idx < 0:
+            seg = M.segment(t, M.replica_of(self.caller))
+            return seg.um_view(loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi)
+        f = self.sched.fetches[src_idx]
+        buf = staged[src_idx]
+        return _capi.UmView(buf.data_ptr(), loc.rows.lo - f.r0, loc.rows.hi - f.r0, loc.cols.lo - f.c0,
+                            loc.cols.hi - f.c0, buf.stride(0), um_dtype(M.dtype), self.dev)
+
+    def _scratch_gemm(self, op, ga, gb):
+        """Unfused remote update: GEMM into zeroed scratch, then K3 accumulate."""
+        lib = _capi.load()
+        m, n = len(op.m_bound), len(op.n_bound)
+        pitch = pitch_for(n, torch.float32)
+        with torch.cuda.stream(self.cs):
+            scratch = torch.zeros((m, pitch), dtype=torch.float32, device=f"cuda:{self.dev}")
+        self.buffers.append(scratch)
+        gs = _capi.UmView(scratch.data_ptr(), 0, m, 0, n, pitch, _capi.UM_F32, self.dev)
+        _capi.check(lib.um_gemm_acc(ctypes.byref(ga), ctypes.byref(gb), ctypes.byref(gs),
+                                    ctypes.c_void_p(self.cs.cuda_stream)), "um_gemm_acc")
+        cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+        dst = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+        with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
+            _capi.check(lib.um_accumulate(ctypes.byref(gs), ctypes.byref(dst), ctypes.c_void_p(self.cs.cuda_stream)),
+                        "um_accumulate")
+        st = self.stats
+        st.launches += 2
+        st.peak_ops_per_launch = max(st.peak_ops_per_launch, 1)
+        st.peak_inflight_accums = max(st.peak_inflight_accums, 1)
+        st.executed_ops.append(op)
+        st.a_requests.append(op.a_tile)
+        st.b_requests.append(op.b_tile)
+
+
+def run_direct(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
+               caller: int) -> RunStats:
+    """Direct execution of one rank's rotated op list (runtime.py:193-256).
+
+    Asynchronous and stream-ordered; the driver (execute_multiply) owns the
+    run-level barrier and the replica reduction, as in the reference.
+    """
+    _check_operands(A, B, C)
+    fab = A.fabric
+    if not fab.is_local(caller):
+        raise ContractError(f"rank {caller} is hosted by process {fab.process_of(caller)}")
+    fab.heap.exchange()
+    sched = lower_direct(A, B, C, cfg, caller)
+    _count_reference_traffic(A, B, C, cfg, sched)
+    run = _RankRun(A, B, C, cfg, sched, _current_events(fab)).issue()
+    _join_current(fab, [run.done])
+    run.stats.flops = int(fab.counters.flops[caller])
+    return run.stats
+
+
+# ---------------------------------------------------------------------------
+# K4: replica reduction
+# ---------------------------------------------------------------------------
+
+def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None):
+    """replica[origin] += sum_{r != origin} replica[r] (in r order), K4 on device.
+
+    distributed: tile rows are split into c slices; slice j is reduced by the
+    GPU of replica j's tile owner (slice `origin` by the origin owner), which
+    pulls that slice from every other replica over NVLink and adds the sum
+    into the origin's slice.
+    """
+    fab = C.fabric
+    fab._require_data()
+    lib = _capi.load()
+    if start_events is None:
+        start_events = _current_events(fab)
+    done = []
+    for t in C.grid.tiles():
+        dst = C.segment(t, origin)
+        if dst.length == 0:
+            continue
+        srcs = [C.segment(t, r) for r in range(C.c) if r != origin]
+        nslices = C.c if distributed else 1
+        rows = dst.rows
+        for j in range(nslices):
+            r0, r1 = rows * j // nslices, rows * (j + 1) // nslices
+            if r1 <= r0:
+                continue
+            reducer = C.owner_rank(t, j) if distributed else dst.owner
+            if not fab.is_local(reducer):
+                continue
+            dev = fab.device_of(reducer)
+            stream = fab.stream(reducer, "reduce")
+            for ev in start_events:
+                stream.wait_event(ev)
+            dv = dst.um_view(r0, r1, 0, dst.cols)
+            sv = (_capi.UmView * len(srcs))(*[s.um_view(r0, r1, 0, s.cols) for s in srcs])
+            with torch.cuda.device(dev):
+                _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), ctypes.c_void_p(stream.cuda_stream)),
+                            "um_reduce_replicas")
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done.append(ev)
+    _join_current(fab, done)
+    if fab.world.size > 1:
+        fab.synchronize()
+    return done
+
+
+# ---------------------------------------------------------------------------
+# IR replay (runtime.py:259-336)
+# ---------------------------------------------------------------------------
+
+def run_ir(prog, graph, A, B, C, cfg: ExecConfig, caller: int) -> RunStats:
+    """Replay a validated single-rank IR program on the device.
+
+    A step's computes run first (grouped K1 launch; remote-C ops into scratch),
+    then its comm: fetches pull whole tiles into the tile cache on the copy
+    stream (satisfying later steps), accumulates push scratch into remote C
+    tiles with K3 after their compute (stream order).
+    """
+    v = lowering.validate(prog, {caller: graph})
+    if v is not None:
+        raise ContractError(f"refusing to run invalid IR: {v.kind}: {v.message}")
+    _check_operands(A, B, C)
+    fab = A.fabric
+    fab.heap.exchange()
+    lib = _capi.load()
+    dev = fab.device_of(caller)
+    gs, cs = fab.stream(caller, "get"), fab.stream(caller, "compute")
+    for ev in _current_events(fab):
+        gs.wait_event(ev)
+        cs.wait_event(ev)
+    mats = {"A": A, "B": B, "C": C}
+    stats = RunStats()
+    cache: dict[int, tuple] = {}          # data node -> (buffer, event)
+    scratch: dict[int, torch.Tensor] = {}
+    keep = []
+    lgp = cfg.accumulate_mode is AccumulateMode.LOCK_GET_PUT
+    ctr = fab.counters
+    with torch.cuda.device(dev):
+        for step in prog.steps_by_rank[caller]:
+            batch = []
+            for i in step.compute:
+                op = graph.ops[i]
+                cn = graph.compute_nodes[i]
+                views = []
+                for d, t, loc, M in ((cn.a_data, op.a_tile, op.a_local, A), (cn.b_data, op.b_tile, op.b_local, B)):
+                    if d in cache:
+                        buf, ev = cache[d]
+                        cs.wait_event(ev)
+                        views.append(_capi.UmView(buf.data_ptr(), loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi,
+                                                  buf.stride(0), um_dtype(M.dtype), dev))
+                    else:
+                        seg = M.segment(t, M.replica_of(caller))
+                        views.append(seg.um_view(loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi))
+                if graph.data_nodes[cn.c_data].local:
+                    cseg = C.segment(op.c_tile, C.replica_of(caller))
+                    gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+                else:
+                    m, n = len(op.m_bound), len(op.n_bound)
+                    with torch.cuda.stream(cs):
+                        sc = torch.zeros((m, pitch_for(n, torch.float32)), dtype=torch.float32, device=f"cuda:{dev}")
+                    scratch[i] = sc
+                    gc = _capi.UmView(sc.data_ptr(), 0, m, 0, n, sc.stride(0), _capi.UM_F32, dev)
+                batch.append(_capi.UmGemmOp(views[0], views[1], gc, 0, 0))
+                ctr.add_flops(caller, op.flops)
+                stats.executed_ops.append(op)
+            if batch:
+                arr = (_capi.UmGemmOp * len(batch))(*batch)
+                _capi.check(lib.um_gemm_acc_batch(arr, len(batch), dev, ctypes.c_void_p(cs.cuda_stream)),
+                            "um_gemm_acc_batch")
+                stats.launches += 1
+                stats.peak_ops_per_launch = max(stats.peak_ops_per_launch, len(batch))
+            for cm in step.comm:
+                M = mats[cm.matrix]
+                if cm.kind == "fetch":
+                    seg = M.segment(cm.tile, M.replica_of(caller))
+                    with torch.cuda.stream(gs):
+                        buf = torch.empty((seg.rows, seg.pitch), dtype=M.dtype, device=f"cuda:{dev}")
+                    buf.record_stream(cs)
+                    src = seg.um_view(0, seg.rows, 0, seg.cols)
+                    dst = _capi.UmView(buf.data_ptr(), 0, seg.rows, 0, seg.cols, seg.pitch, um_dtype(M.dtype), dev)
+                    _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(gs.cuda_stream)),
+                                "um_get")
+                    ev = torch.cuda.Event()
+                    ev.record(gs)
+                    cache[cm.data] = (buf, ev)
+                    keep.append(buf)
+                    ctr.add_traffic(caller, seg.owner, ELEM_BYTES * seg.length, 1, seg.length * buf.element_size())
+                    stats.gets += 1
+                    (stats.a_requests if cm.matrix == "A" else stats.b_requests).append(cm.tile)
+                else:
+                    op = graph.ops[cm.op_index]
+                    sc = scratch.pop(cm.op_index)
+                    keep.append(sc)
+                    cseg = C.segment(op.c_tile, C.replica_of(caller))
+                    m, n = len(op.m_bound), len(op.n_bound)
+                    src = _capi.UmView(sc.data_ptr(), 0, m, 0, n, sc.stride(0), _capi.UM_F32, dev)
+                    dst = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+                    _capi.check(lib.um_accumulate(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(cs.cuda_stream)),
+                                "um_accumulate")
+                    full = len(op.c_local.cols) == len(C.tile_bounds(op.c_tile).cols)
+                    msgs = 1 if full else m
+                    ctr.add_traffic(caller, cseg.owner, (2 if lgp else 1) * ELEM_BYTES * m * n,
+                                    (2 if lgp else 1) * msgs, 4 * m * n)
+                    stats.peak_inflight_accums = max(stats.peak_inflight_accums, 1)
+        for buf, ev in cache.values():
+            cs.wait_event(ev)
+        done = torch.cuda.Event()
+        done.record(cs)
+    _join_current(fab, [done])
+    stats.pool_acquired = stats.pool_released = stats.pool_peak = stats.gets
+    stats.peak_inflight_gemms = 1 if stats.executed_ops else 0
+    stats.flops = int(ctr.flops[caller])
+    return stats
+
+
+# ---------------------------------------------------------------------------
+# whole-multiply driver (runtime.py:339-387)
+# ---------------------------------------------------------------------------
+
+def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
+                     execution: str = "direct", machine=None, max_compute: int | None = None,
+                     max_comm: int | None = None, threaded: bool = False) -> dict[int, RunStats]:
+    """Run every (local) rank, barrier, then reduce replicated C into replica 0.
+
+    execution: "direct" | "ir:greedy" | "ir:cost" | "ir:exhaustive".
+    All ranks are issued asynchronously on their own streams (co-resident
+    ranks overlap); `threaded` is accepted for API parity.
+    """
+    if execution not in ("direct", "ir:greedy", "ir:cost", "ir:exhaustive"):
+        raise ValueError(f"unknown execution mode {execution!r}")
+    _check_operands(A, B, C)
+    fab = A.fabric
+    fab.heap.exchange()
+    ranks = fab.local_ranks()
+    results: dict[int, RunStats] = {}
+    start = _current_events(fab)
+    done = []
+    if execution == "direct":
+        runs = []
+        for r in ranks:
+            sched = lower_direct(A, B, C, cfg, r)
+            _count_reference_traffic(A, B, C, cfg, sched)
+            runs.append(_RankRun(A, B, C, cfg, sched, start).issue())
+        for run in runs:
+            run.stats.flops = int(fab.counters.flops[run.caller])
+            results[run.caller] = run.stats
+            done.append(run.done)
+    else:
+        mats = {"A": A, "B": B, "C": C}
+        for r in ranks:
+            ops = opgen.generate(cfg.stationarity, A, B, C, r)
+            g = lowering.build_graph(ops, mats, r)
+            if execution == "ir:greedy":
+                prog = lowering.lower_greedy(g, max_compute, max_comm)
+            elif execution == "ir:cost":
+                prog = lowering.lower_cost_greedy(g, machine, max_compute, max_comm)
+            else:
+                prog = lowering.lower_exhaustive(g, machine, max_compute, max_comm)
+            results[r] = run_ir(prog, g, A, B, C, cfg, r)
+        done = _current_events(fab)
+    if fab.world.size > 1:
+        fab.synchronize()            # run-level barrier across processes
+    if C.c > 1:
+        reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done)
+        for t in C.grid.tiles():      # reference-model accounting of the pulls
+            dst = C.segment(t, 0)
+            for r in range(1, C.c):
+                src = C.segment(t, r)
+                if src.length:
+                    fab.counters.add_traffic(dst.owner, src.owner, ELEM_BYTES * src.length, 1, 4 * src.length)
+    else:
+        _join_current(fab, done)
+    return results
