@@ -1,0 +1,342 @@
+"""Benchmark: distributed GEMM bf16 TFLOP/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl b200|reference]
+
+One step = one full `execute_multiply` (every get, GEMM, remote accumulate and
+replica reduction of the configuration) over synthetic operands resident in
+HBM.  N=1 runs BASELINE configs[1] (cfg2: 1D row-block A and C, B replicated,
+m=65536, n=k=8192) as its single-GPU instance (p = 1 rank); under torchrun
+(N>1) every process hosts one logical rank (p = N) of the same global
+problem, so total work is fixed ("strong" scaling).
+
+Printed JSON keys follow the driver contract; `value` is device-timed
+(CUDA events, max over ranks), `e2e` repeats the metric through the public
+API with pinned host buffers (H2D of A/B and D2H of C inside the timed
+region), `roofline` relates the dominant kernel (K1) to the measured bf16
+peak, `cpu_baseline` times the CPU oracle port (tests-only code, used here
+only as the reference arm) on a bounded sample on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (m, n, k, a_part, b_part, c_part, c_a(p), c_b(p), c_c(p), description)
+    "cfg1": (1024, 1024, 1024, "2d", "2d", "2d", lambda p: 1, lambda p: 1, lambda p: 1,
+             "2D block A/B/C, m=n=k=1024"),
+    "cfg2": (65536, 8192, 8192, "row", "2d", "row", lambda p: 1, lambda p: p, lambda p: 1,
+             "1D row-block A and C, B replicated (sequence-parallel), m=65536 n=k=8192"),
+    "cfg3": (8192, 8192, 65536, "col", "row", "2d", lambda p: 1, lambda p: 1, lambda p: p,
+             "A col / B row outer product, C replicated (Megatron-TP), m=n=8192 k=65536"),
+    "cfg4": (16384, 16384, 16384, "2d", "2d", "2d", lambda p: min(2, p), lambda p: min(2, p), lambda p: min(2, p),
+             "2.5D: 2D block A/B/C with c=2, 16384^3"),
+    "cfg5": (16384, 16384, 16384, "2d", "col", "row", lambda p: 1, lambda p: 1, lambda p: 1,
+             "mismatched: A 2D, B col, C row, 16384^3"),
+}
+
+METRIC = "distributed GEMM bf16 TFLOP/s at 1/2/4/8 B200 and % of tensor-core peak"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["bf16_tflops"]), float(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])), "measured"
+    except Exception:  # noqa: BLE001
+        return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(m, n, k, p, desc, target_s: float):
+    """Time the CPU oracle port (numpy fp64, all host threads) on a row sample.
+
+    Returns (tflops, sample description, cores, seconds)."""
+    import numpy as np
+
+    from oracle import um_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    rows = 64
+    rng = np.random.default_rng(0)
+
+    def run(rows):
+        a = rng.uniform(-1, 1, size=(rows, k))
+        b = rng.uniform(-1, 1, size=(k, n))
+        mats = [O.Mat("A", rows, k, O.Spec(rows, k, 1, 1), 1, 1), O.Mat("B", k, n, O.Spec(k, n, 1, 1), 1, 1),
+                O.Mat("C", rows, n, O.Spec(rows, n, 1, 1), 1, 1)]
+        t0 = time.perf_counter()
+        O.execute("c", *mats, a, b)
+        return time.perf_counter() - t0
+
+    dt = run(rows)
+    rows = int(min(m, max(64, rows * target_s / max(dt, 1e-3))))
+    dt = run(rows)
+    flops = 2.0 * rows * n * k
+    return flops / dt / 1e12, f"{rows}x{n}x{k} row sample of {desc} (fp64 numpy oracle port)", cores, dt
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle port on this host's cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    m, n, k, ap, bp, cp, fa, fb, fc, desc = CONFIGS[args.config]
+    import numpy as np
+
+    from oracle import um_oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    rate, sample, cores, dt = cpu_oracle_rate(m, n, k, args.gpus, desc, target_s=args.ref_step_s)
+    rows = int(sample.split("x")[0])
+    rng = np.random.default_rng(1)
+    a = rng.uniform(-1, 1, size=(rows, k))
+    b = rng.uniform(-1, 1, size=(k, n))
+    mats = [O.Mat("A", rows, k, O.Spec(rows, k, 1, 1), 1, 1), O.Mat("B", k, n, O.Spec(k, n, 1, 1), 1, 1),
+            O.Mat("C", rows, n, O.Spec(rows, n, 1, 1), 1, 1)]
+    for _ in range(args.warmup):
+        O.execute("c", *mats, a, b)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.execute("c", *mats, a, b)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = 2.0 * rows * n * k / dt / 1e12
+    out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config}: {desc}", "m": m, "n": n, "k": k, "p": args.gpus,
+                      "partitions": [ap, bp, cp], "sample_rows": rows},
+           "impl": "reference",
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def b200_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08874_b200 import ExecConfig, execute_multiply
+    from paper_2510_08874_b200 import runtime as rt
+    from paper_2510_08874_b200.cli import build_problem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    p = world
+    m, n, k, ap, bp, cp, fa, fb, fc, desc = CONFIGS[args.config]
+    ca, cb, cc = fa(p), fb(p), fc(p)
+    fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, ca, cb, cc, seed=0, real=True, synthetic=True,
+                                       devices=[local] if world > 1 else [0])
+    cfg = ExecConfig()
+    flops = 2.0 * m * n * k
+    dev = torch.device(f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timing
+    for _ in range(args.warmup):
+        execute_multiply(A, B, C, cfg)
+    barrier()
+    rt.TRACE.clear()
+    rt.TRACE_ENABLED = True
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    launches = 0
+    for _ in range(args.steps):
+        stats = execute_multiply(A, B, C, cfg)
+        launches += sum(s.launches for s in stats.values()) + (len(list(C.grid.tiles())) if C.c > 1 else 0)
+    e1.record()
+    barrier()
+    clocks = sampler.stop()
+    rt.TRACE_ENABLED = False
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    value = flops / (ms * 1e-3) / 1e12
+    # dominant kernel (K1 grouped launch) durations, measured on its own stream
+    durs = [s.elapsed_time(e) for s, e, _ in rt.TRACE]
+    kflops = [f for _, _, f in rt.TRACE]
+    peak, peak_sus, peak_kind = load_peaks()
+    if durs:
+        achieved = sum(kflops) / (sum(durs) * 1e-3) / 1e12
+    else:
+        achieved = None
+
+    # ---- end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks)
+
+    # ---- CPU baseline (oracle port) on rank 0, N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, sample, cores, _ = cpu_oracle_rate(m, n, k, p, desc, target_s=args.cpu_s)
+        cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "config": {"workload": f"{args.config}: {desc}", "m": m, "n": n, "k": k, "p": p,
+                          "partitions": [ap, bp, cp], "replication": [ca, cb, cc], "stationarity": "c",
+                          "inputs": "bf16 uniform(-1,1) generated on device (K5), C fp32",
+                          "l2": "inputs larger than L2 (A %.0f MiB, C %.0f MiB per rank > 126 MB)" % (
+                              m * k * 2 / p / 2**20, m * n * 4 / p / 2**20)},
+               "frac_of_peak": value / (world * peak), "peak_per_gpu_tflops": peak, "peak_kind": peak_kind,
+               "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                            "frac": (achieved / peak) if achieved else None, "traffic": None,
+                            "kernel": "um::gemm::gemm_bf16_kernel<2>", "launches_timed": len(durs),
+                            "algorithmic_flops_per_launch": (sum(kflops) / len(kflops)) if kflops else None},
+               "clocks": clocks, "gpu_launches": launches,
+               "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
+    """Same metric via the public API from pinned host buffers (H2D A,B; D2H C)."""
+    import torch
+
+    from paper_2510_08874_b200 import execute_multiply
+
+    def local_tiles(M):
+        out = []
+        for (rep, t), seg in M._segments.items():
+            if seg.storage is not None and seg.length:
+                out.append(seg)
+        return out
+
+    a_segs, b_segs, c_segs = local_tiles(A), local_tiles(B), local_tiles(C)
+    host_a = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in a_segs]
+    host_b = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in b_segs]
+    host_c = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in c_segs]
+    for h in host_a + host_b:
+        h.uniform_(-1, 1)
+    h2d = sum(h.numel() * h.element_size() for h in host_a + host_b)
+    d2h = sum(h.numel() * h.element_size() for h in host_c)
+
+    def step():
+        for s, h in zip(a_segs + b_segs, host_a + host_b):
+            s.view2d().copy_(h, non_blocking=True)
+        execute_multiply(A, B, C, cfg)
+        for s, h in zip(c_segs, host_c):
+            h.copy_(s.view2d(), non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    steps = max(1, args.steps // 2)
+    for _ in range(steps):
+        step()
+    e1.record()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")
+    ap.add_argument("--ref-step-s", type=float, default=4.0, help="target seconds per reference-arm step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

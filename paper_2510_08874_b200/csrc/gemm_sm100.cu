@@ -363,10 +363,13 @@ static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int
 
 // TMA requires the innermost start coordinate of a box to be 16-byte aligned
 // (measured: an unaligned column offset raises an illegal-instruction fault;
-// row offsets are free).  Slices of misaligned partitionings (e.g. 3x4 tiles,
+// row offsets are free), and a 16-byte aligned base and row pitch.  Slices of misaligned partitionings (e.g. 3x4 tiles,
 // cli.py:151-152) therefore get their A/B slice staged into an aligned scratch
 // and their C update routed through the pointer-based red.global epilogue.
-static inline bool inner_aligned(const um_view& v) { return (v.col_lo * esize(v.dtype)) % 16 == 0; }
+static inline bool inner_aligned(const um_view& v) {
+  const int64_t es = esize(v.dtype);
+  return (v.col_lo * es) % 16 == 0 && (v.pitch * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(v.base) & 15) == 0;
+}
 static inline int64_t aligned_pitch(int64_t cols, int32_t dtype) {
   const int64_t per16 = 16 / esize(dtype);
   return (cols + per16 - 1) / per16 * per16;

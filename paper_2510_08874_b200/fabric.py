@@ -232,7 +232,8 @@ class Fabric:
     queries work, any data movement raises.
     """
 
-    def __init__(self, nprocs: int, links: LinkTable | None = None, devices=None, process_group=None):
+    def __init__(self, nprocs: int, links: LinkTable | None = None, devices=None, process_group=None,
+                 device_api=None):
         if nprocs < 1:
             raise ValueError("need at least one process")
         self.nprocs = nprocs
@@ -250,7 +251,7 @@ class Fabric:
         if not self.placement_only and self.world.size == 1 and len(self.devices) > 1:
             arr = (ctypes.c_int32 * len(self.devices))(*self.devices)
             _capi.check(_capi.load().um_init(len(self.devices), arr), "um_init")
-        self.heap = _heap.SymmetricHeap(self)
+        self.heap = _heap.SymmetricHeap(self, device_api)
         self._streams: dict = {}
 
     # -- placement ---------------------------------------------------------------

@@ -41,6 +41,11 @@ from paper_2510_08874_b200.fabric import ELEM_BYTES, AccumulateMode, pitch_for, 
 from paper_2510_08874_b200.opgen import LocalMatMulOp, Stationarity
 from paper_2510_08874_b200.tiling import TileIdx
 
+# Launch tracing for the benchmark's roofline: (start, end, algorithmic flops)
+# CUDA events recorded on the compute stream around every grouped K1 launch.
+TRACE: list = []
+TRACE_ENABLED = False
+
 __all__ = ["ExecConfig", "BufferPool", "RunStats", "iteration_offset", "local_gemm", "run_direct",
            "run_ir", "execute_multiply", "reduce_replicas", "lower_direct", "DirectSchedule"]
 
@@ -346,8 +351,15 @@ class _RankRun:
                 if not batch:
                     return
                 arr = (_capi.UmGemmOp * len(batch))(*batch)
+                if TRACE_ENABLED:
+                    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    t0.record(self.cs)
                 _capi.check(lib.um_gemm_acc_batch(arr, len(batch), self.dev, ctypes.c_void_p(self.cs.cuda_stream)),
                             "um_gemm_acc_batch")
+                if TRACE_ENABLED:
+                    t1.record(self.cs)
+                    TRACE.append((t0, t1, float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo)
+                                                    * (g.b.col_hi - g.b.col_lo) for g in batch))))
                 st.launches += 1
                 st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
                 st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)

@@ -1,0 +1,111 @@
+"""K1 (tcgen05 GEMM) through the kernel plugin: c += a @ b on B200.
+
+Integer-valued inputs are exact in bf16 and every fp32 partial sum stays
+below 2**24, so results must be BIT-EXACT against an fp32 reference of the
+same op; real inputs are held to a normalised error of 1e-5 (the north-star
+gate is 1e-3)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import um_oracle as O
+from paper_2510_08874_b200 import kernels
+from paper_2510_08874_b200.errors import ContractError
+
+pytestmark = pytest.mark.gpu
+
+
+def ints(rows, cols, gen, dtype, pad=0):
+    t = torch.randint(-8, 9, (rows, cols + pad), generator=gen, device="cuda").to(dtype)
+    return t
+
+
+def ref_acc(c0, a, b):
+    return c0 + (a.double() @ b.double()).float()
+
+
+CASES = [
+    # m, n, k, (a row/col offset, b row/col offset, c row/col offset)
+    (128, 256, 64, (0, 0, 0, 0, 0, 0)),
+    (256, 256, 64, (0, 0, 0, 0, 0, 0)),
+    (7, 9, 5, (0, 0, 0, 0, 0, 0)),
+    (1, 1, 1, (0, 0, 0, 0, 0, 0)),
+    (1000, 1000, 1000, (0, 0, 0, 0, 0, 0)),
+    (300, 200, 100, (5, 8, 7, 16, 2, 4)),         # row offsets free, aligned column offsets
+    (300, 200, 100, (5, 3, 7, 11, 2, 1)),         # misaligned column offsets (staged / red path)
+    (513, 257, 129, (1, 0, 0, 0, 3, 0)),
+    (2048, 4096, 2048, (2048, 0, 0, 0, 0, 0)),    # cfg5-shaped op slice
+    (64, 8192, 4096, (0, 0, 0, 0, 0, 0)),
+]
+
+
+@pytest.mark.parametrize("m,n,k,off", CASES)
+def test_integer_exact(cuda, m, n, k, off):
+    g = torch.Generator(device="cuda").manual_seed(m * 31 + n * 7 + k)
+    ar, ac, br, bc, cr, cc = off
+    A = ints(ar + m + 3, ac + k, g, torch.bfloat16, pad=5)
+    B = ints(br + k + 2, bc + n, g, torch.bfloat16, pad=3)
+    C = ints(cr + m + 1, cc + n, g, torch.float32, pad=7)
+    a, b, c = A[ar:ar + m, ac:ac + k], B[br:br + k, bc:bc + n], C[cr:cr + m, cc:cc + n]
+    expect = ref_acc(c.clone(), a, b)
+    before = C.clone()
+    kernels.gemm_accumulate(a, b, c)
+    torch.cuda.synchronize()
+    assert torch.equal(c, expect)
+    mask = torch.ones_like(C, dtype=torch.bool)
+    mask[cr:cr + m, cc:cc + n] = False
+    assert torch.equal(C[mask], before[mask]), "wrote outside the C slice"
+
+
+def test_real_inputs_tolerance(cuda):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, n, k = 1024, 768, 4096
+    a = (torch.rand(m, k, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    b = (torch.rand(k, n, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    c = torch.zeros(m, n, device="cuda")
+    kernels.gemm_accumulate(a, b, c)
+    ref = (a.double() @ b.double()).cpu().numpy()
+    err = O.max_normalized_error(c.cpu().numpy(), ref, a.double().cpu().numpy(), b.double().cpu().numpy())
+    assert err < 1e-5, err
+
+
+def test_accumulates_repeatedly(cuda):
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = ints(384, 320, g, torch.bfloat16)
+    b = ints(320, 512, g, torch.bfloat16)
+    c = torch.zeros(384, 512, device="cuda")
+    for _ in range(3):
+        kernels.gemm_accumulate(a, b, c)
+    assert torch.equal(c, 3 * (a.double() @ b.double()).float())
+
+
+def test_contract_errors(cuda):
+    a = torch.zeros(4, 4, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        kernels.gemm_accumulate(a, a[:3], torch.zeros(4, 4, device="cuda"))
+    with pytest.raises(ContractError):
+        kernels.gemm_accumulate(a.float(), a, torch.zeros(4, 4, device="cuda"))
+    with pytest.raises(ContractError):
+        kernels.gemm_accumulate(a.cpu(), a.cpu(), torch.zeros(4, 4))
+
+
+def test_one_cta_variant_matches(cuda):
+    """The cta_group::1 kernel (UM_GEMM_CG=1) gives the same exact results."""
+    code = (
+        "import torch,sys; sys.path.insert(0,'.');"
+        "from paper_2510_08874_b200 import kernels;"
+        "g=torch.Generator(device='cuda').manual_seed(3);"
+        "a=torch.randint(-8,9,(700,900),generator=g,device='cuda').to(torch.bfloat16);"
+        "b=torch.randint(-8,9,(900,600),generator=g,device='cuda').to(torch.bfloat16);"
+        "c=torch.zeros(700,600,device='cuda'); kernels.gemm_accumulate(a,b,c);"
+        "assert torch.equal(c,(a.double()@b.double()).float()); print('OK')")
+    env = dict(os.environ, UM_GEMM_CG="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]

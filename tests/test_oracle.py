@@ -139,3 +139,18 @@ def test_round_bf16():
     import torch
 
     assert np.array_equal(r, torch.tensor(x).to(torch.bfloat16).float().numpy())
+
+
+def test_reference_compiled_kernel_agrees(runtime_golden, numeric_golden):
+    """oracle/_ref (the reference's own _gemmcore, built from /root/reference) gives
+    the same results as the numpy port on the golden integer cases."""
+    try:
+        O.gemm_kernel("reference")
+    except ImportError:
+        pytest.skip("oracle/_ref not built")
+    for i, meta in enumerate(runtime_golden["numeric"][:6]):
+        p, m, n, k, ap, bp, cp, ca, cb, cc, stat, real = meta["case"]
+        M = mats(dict(p=p, m=m, n=n, k=k, a_part=ap, b_part=bp, c_part=cp, c_a=ca, c_b=cb, c_c=cc))
+        a, b = numeric_golden[f"a{i}"], numeric_golden[f"b{i}"]
+        got = O.execute(stat, M["A"], M["B"], M["C"], a, b, kernel="reference")
+        assert np.array_equal(np.stack(got), numeric_golden[f"final{i}"])
