@@ -187,9 +187,14 @@ def b200_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    local = local % ndev          # several ranks may share a GPU (e.g. 2 ranks on a 1-GPU box)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
     p = world
     m, n, k, ap, bp, cp, fa, fb, fc, desc = CONFIGS[args.config]
     ca, cb, cc = fa(p), fb(p), fc(p)
@@ -207,7 +212,8 @@ def b200_arm(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -275,33 +281,28 @@ def b200_arm(args):
 
 
 def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
-    """Same metric via the public API from pinned host buffers (H2D A,B; D2H C)."""
+    """Same metric through the public host-memory API (hostio.multiply_from_host):
+    every step uploads A and B from pinned host buffers and downloads C, with the
+    transfers pipelined against the GEMMs over row panels."""
     import torch
 
-    from paper_2510_08874_b200 import execute_multiply
+    from paper_2510_08874_b200.hostio import multiply_from_host
 
-    def local_tiles(M):
-        out = []
-        for (rep, t), seg in M._segments.items():
-            if seg.storage is not None and seg.length:
-                out.append(seg)
-        return out
+    m, k = A.global_shape.rows, A.global_shape.cols
+    n = B.global_shape.cols
+    a_h = torch.empty((m, k), dtype=A.dtype, pin_memory=True).uniform_(-1, 1)
+    b_h = torch.empty((k, n), dtype=B.dtype, pin_memory=True).uniform_(-1, 1)
+    c_h = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
 
-    a_segs, b_segs, c_segs = local_tiles(A), local_tiles(B), local_tiles(C)
-    host_a = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in a_segs]
-    host_b = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in b_segs]
-    host_c = [torch.empty(s.view2d().shape, dtype=s.dtype, pin_memory=True) for s in c_segs]
-    for h in host_a + host_b:
-        h.uniform_(-1, 1)
-    h2d = sum(h.numel() * h.element_size() for h in host_a + host_b)
-    d2h = sum(h.numel() * h.element_size() for h in host_c)
+    def nbytes(M, replica0_only=False):
+        return sum(seg.length * seg.esize for (rep, t), seg in M._segments.items()
+                   if seg.storage is not None and (rep == 0 or not replica0_only))
+
+    h2d = nbytes(A) + nbytes(B)
+    d2h = nbytes(C, replica0_only=True)
 
     def step():
-        for s, h in zip(a_segs + b_segs, host_a + host_b):
-            s.view2d().copy_(h, non_blocking=True)
-        execute_multiply(A, B, C, cfg)
-        for s, h in zip(c_segs, host_c):
-            h.copy_(s.view2d(), non_blocking=True)
+        multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -315,7 +316,8 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps)
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "api": "hostio.multiply_from_host",
+            "panels": args.panels}
 
 
 def main():
@@ -326,6 +328,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--panels", type=int, default=8, help="row panels of the host-streaming e2e path")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="target seconds per reference-arm step")

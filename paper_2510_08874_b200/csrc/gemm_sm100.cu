@@ -46,7 +46,7 @@ constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
-constexpr int GROUP_M = 16;   // rasterisation group (tiles of BM*CG rows)
+constexpr int GROUP_M = 16;   // default rasterisation group (tiles of BM*CG rows); UM_GEMM_GROUP overrides
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 
 template <int CG>
@@ -69,7 +69,7 @@ struct alignas(16) Work {
   int32_t a_row0, a_col0;
   int32_t b_row0, b_col0;
   int32_t c_row0, c_col0;
-  int32_t c_vec_ok, pad0;
+  int32_t c_vec_ok, group;
   int64_t c_pitch;
   float* c_ptr;
 };
@@ -80,14 +80,29 @@ __device__ __forceinline__ int find_work(const Work* works, int nwork, int t) {
   return w;
 }
 
+// Rasterisation: tiles are walked in groups of `group` consecutive m-tiles
+// (group > 0) or n-tiles (group < 0), the other dimension sweeping inside a
+// group, so a wave of clusters shares operand panels in L2.
 __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int& nb) {
-  const int group = GROUP_M * wk.tiles_n;
-  const int g = lt / group;
-  const int first_m = g * GROUP_M;
-  const int gm = min(wk.tiles_m - first_m, GROUP_M);
-  const int r = lt - g * group;
-  mb = first_m + r % gm;
-  nb = r / gm;
+  if (wk.group >= 0) {
+    const int G = wk.group;
+    const int span = G * wk.tiles_n;
+    const int g = lt / span;
+    const int first = g * G;
+    const int gm = min(wk.tiles_m - first, G);
+    const int r = lt - g * span;
+    mb = first + r % gm;
+    nb = r / gm;
+  } else {
+    const int G = -wk.group;
+    const int span = G * wk.tiles_m;
+    const int g = lt / span;
+    const int first = g * G;
+    const int gn = min(wk.tiles_n - first, G);
+    const int r = lt - g * span;
+    nb = first + r % gn;
+    mb = r / gn;
+  }
 }
 
 template <int CG>
@@ -236,7 +251,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else ptx::mbar_arrive_cluster(&tmem_empty[as], 0);
           }
         }
-        if (!wk.c_remote) {
+        if (wk.c_remote == 3) {
+          // (profiling only) accumulator dropped: isolates the main loop's cost
+        } else if (wk.c_remote != 1) {
           // registers -> swizzled smem box -> TMA reduce-add into C
           if (lane == 0) ptx::bulk_wait_read<1>();
           __syncwarp();
@@ -249,8 +266,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_reduce_add_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
-                                   wk.c_row0 + row_in_op);
+            if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
+              ptx::tma_store_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
+                                wk.c_row0 + row_in_op);
+            else
+              ptx::tma_reduce_add_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
+                                     wk.c_row0 + row_in_op);
             ptx::bulk_commit();
           }
           buf ^= 1;
@@ -318,6 +339,17 @@ static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint
     return fail(UM_ECUDA, std::string("cuTensorMapEncodeTiled failed for ") + what + " (code " +
                               std::to_string((int)r) + ")");
   return UM_OK;
+}
+
+static int raster_group() {
+  static int g = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("UM_GEMM_GROUP");
+    g = e ? atoi(e) : GROUP_M;
+    if (g == 0) g = GROUP_M;
+  });
+  return g;
 }
 
 static int g_cta_group = 2;  // default kernel variant; UM_GEMM_CG=1 env selects the 1-CTA kernel
@@ -453,6 +485,12 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.num_kb = (int32_t)((k + BK - 1) / BK);
     w.tile_start = total;
     w.c_remote = op.c_remote;
+    if (!op.c_remote) {
+      // profiling knob: UM_GEMM_EPI_DEBUG=store|none replaces the reduce-add
+      static const char* dbg = getenv("UM_GEMM_EPI_DEBUG");
+      if (dbg && !strcmp(dbg, "store")) w.c_remote = 2;
+      if (dbg && !strcmp(dbg, "none")) w.c_remote = 3;
+    }
     w.a_row0 = (int32_t)op.a.row_lo;
     w.a_col0 = (int32_t)op.a.col_lo;
     w.b_row0 = (int32_t)op.b.row_lo;
@@ -461,6 +499,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.c_col0 = (int32_t)op.c.col_lo;
     w.c_pitch = op.c.pitch;
     w.c_ptr = reinterpret_cast<float*>(op.c.base);
+    w.group = raster_group();
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
     total += w.tiles_m * w.tiles_n;
     CUtensorMap ma, mbm, mc;

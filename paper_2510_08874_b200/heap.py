@@ -58,6 +58,22 @@ class World:
 
             dist.barrier(group=self.group)
 
+    def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        """Element-wise sum over processes (used by the collective gather)."""
+        if self.size == 1:
+            return t
+        import torch.distributed as dist
+
+        backend = dist.get_backend(self.group)
+        if backend == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+            x = t.to(dev)
+            dist.all_reduce(x, group=self.group)
+            return x.to(t.device)
+        x = t.cpu()
+        dist.all_reduce(x, group=self.group)
+        return x.to(t.device)
+
     def all_gather_object(self, obj):
         if self.size == 1:
             return [obj]

@@ -201,12 +201,21 @@ def _in_place(fabric, owner: int, caller: int, cfg: ExecConfig) -> bool:
     return False
 
 
-def lower_direct(A, B, C, cfg: ExecConfig, caller: int) -> DirectSchedule:
-    """Rotated op list + fetch-once staging plan (host-side, no device work)."""
+def rotated_ops(A, B, C, cfg: ExecConfig, caller: int) -> list:
+    """The caller's op list in execution order (runtime.py:207,213-214)."""
     ops = opgen.generate(cfg.stationarity, A, B, C, caller)
     if ops:
         s = iteration_offset(ops[0].stationary_tile(cfg.stationarity), len(ops))
         ops = ops[s:] + ops[:s]
+    return ops
+
+
+def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None) -> DirectSchedule:
+    """Rotated op list + fetch-once staging plan (host-side, no device work).
+
+    `ops` overrides the planner's list (e.g. ops restricted to a row panel)."""
+    if ops is None:
+        ops = rotated_ops(A, B, C, cfg, caller)
     fabric = A.fabric
     fetches: list[_Fetch] = []
     index: dict = {}
@@ -456,7 +465,8 @@ def run_direct(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix,
 # K4: replica reduction
 # ---------------------------------------------------------------------------
 
-def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None):
+def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None,
+                    rows: tuple[int, int] | None = None):
     """replica[origin] += sum_{r != origin} replica[r] (in r order), K4 on device.
 
     distributed: tile rows are split into c slices; slice j is reduced by the
@@ -476,9 +486,14 @@ def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = T
             continue
         srcs = [C.segment(t, r) for r in range(C.c) if r != origin]
         nslices = C.c if distributed else 1
-        rows = dst.rows
+        lo, hi = 0, dst.rows
+        if rows is not None:     # restrict to a global row window
+            tb = C.tile_bounds(t)
+            lo, hi = max(rows[0], tb.rows.lo) - tb.rows.lo, min(rows[1], tb.rows.hi) - tb.rows.lo
+            if hi <= lo:
+                continue
         for j in range(nslices):
-            r0, r1 = rows * j // nslices, rows * (j + 1) // nslices
+            r0, r1 = lo + (hi - lo) * j // nslices, lo + (hi - lo) * (j + 1) // nslices
             if r1 <= r0:
                 continue
             reducer = C.owner_rank(t, j) if distributed else dst.owner
