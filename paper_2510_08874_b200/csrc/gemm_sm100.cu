@@ -18,17 +18,25 @@
 //    the innermost start coordinate 16-byte aligned; the rare slices that
 //    violate it (misaligned partitionings) are staged (see launch_batch).
 //  * A is row-major m x k -> K-major SW128; B is row-major k x n -> MN-major SW128.
-//  * accumulators live in TMEM (2 x BN fp32 columns, double-buffered so the
-//    epilogue of tile i overlaps the main loop of tile i+1).
+//  * CG == 2: a CTA pair (cluster of 2) issues cta_group::2 UMMA with M = 256;
+//    each CTA stages its 128 rows of A and its half of every B column block.
+//  * tile width NT per CTA pair: 256 (one N=256 accumulator, TMEM double
+//    buffered so the epilogue of tile i overlaps the main loop of tile i+1) or
+//    512 (two N=256 accumulators filling TMEM: 25% fewer operand bytes per
+//    flop through L2; the MMA issuer runs the first k-blocks of a tile on
+//    accumulator 0 while the epilogue still drains accumulator 1, so most of
+//    the drain stays hidden).
 //  * epilogue: tcgen05.ld -> registers -> swizzled smem -> TMA reduce-add
 //    (cp.reduce.async.bulk.tensor ... add) into the local C tile, or
 //    red.global.add.v4.f32 straight into a peer C tile (fused K3).
-//  * CG == 2: a CTA pair (cluster of 2) issues cta_group::2 UMMA of 256 x BN;
-//    each CTA stages half of A (its 128 rows) and half of B (BN/2 columns).
+//  * L2: tiles are walked in groups of m-tiles; the operand reused across the
+//    group is loaded evict_last, the streamed one evict_first.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -41,25 +49,30 @@ namespace um {
 namespace gemm {
 
 constexpr int BM = 128;       // rows per CTA (UMMA M = BM * CG)
-constexpr int BN = 256;       // columns per tile (UMMA N)
+constexpr int UMMA_N = 256;   // columns per tcgen05.mma (one accumulator)
 constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
-constexpr int GROUP_M = 16;   // default rasterisation group (tiles of BM*CG rows); UM_GEMM_GROUP overrides
+constexpr int GROUP_M = 32;   // default rasterisation group (m-tiles); UM_GEMM_GROUP overrides
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
+constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
 
-template <int CG>
+template <int CG, int NT>
 struct Cfg {
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int B_COLS = BN / CG;                    // B columns staged per CTA
-  static constexpr int A_BYTES = BM * BK * 2;               // 16 KiB
-  static constexpr int B_BYTES = BK * B_COLS * 2;           // 32 KiB (CG1) / 16 KiB (CG2)
+  static constexpr int NACC = NT / UMMA_N;                   // accumulators per tile
+  static constexpr int NBUF = 2 / NACC;                      // TMEM tile buffers
+  static constexpr int STAGES = (CG == 2 && NT == 256) ? 6 : 4;
+  static constexpr int SUB_PER_ACC = UMMA_N / CG / 64;       // 64-col B sub-tiles per accumulator per CTA
+  static constexpr int B_SUBS = NACC * SUB_PER_ACC;
+  static constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
+  static constexpr int B_BYTES = B_SUBS * SUB_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BOX_BYTES;
   static constexpr int BAR_BYTES = 256;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;             // two accumulator buffers
+  static constexpr uint32_t TMEM_COLS = 512;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
 struct alignas(16) Work {
@@ -70,6 +83,7 @@ struct alignas(16) Work {
   int32_t b_row0, b_col0;
   int32_t c_row0, c_col0;
   int32_t c_vec_ok, group;
+  int32_t a_pol, b_pol;     // L2 policy: 0 normal, 1 evict_first, 2 evict_last
   int64_t c_pitch;
   float* c_ptr;
 };
@@ -105,21 +119,21 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
   }
 }
 
-template <int CG>
+template <int CG, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_kernel(const Work* __restrict__ works, const CUtensorMap* __restrict__ maps, int nwork,
                      int total_tiles) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::STAGES * C::A_BYTES;
   uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + C::EPI_BYTES);
-  uint64_t* full = bars;                    // [STAGES]
-  uint64_t* empty = bars + C::STAGES;       // [STAGES]
-  uint64_t* tmem_full = bars + 2 * C::STAGES;      // [2]
-  uint64_t* tmem_empty = bars + 2 * C::STAGES + 2; // [2]
+  uint64_t* full = bars;                            // [STAGES]
+  uint64_t* empty = bars + C::STAGES;               // [STAGES]
+  uint64_t* tmem_full = bars + 2 * C::STAGES;       // [NBUF]
+  uint64_t* tmem_empty = bars + 2 * C::STAGES + 2;  // [2]: per buffer (NACC=1) or per accumulator (NACC=2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
 
   const int warp = threadIdx.x / 32;
@@ -147,9 +161,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer (one thread) =====================
+    // ===================== TMA producer (one thread per CTA) =====================
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_normal();
+      const uint64_t pols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
@@ -157,10 +171,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const Work& wk = works[w];
         const CUtensorMap* ma = &maps[3 * w + 0];
         const CUtensorMap* mbm = &maps[3 * w + 1];
+        const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
         int mb, nb;
         tile_coords(wk, t - wk.tile_start, mb, nb);
         const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
-        const int bcol = wk.b_col0 + nb * BN + (int)cta_rank * C::B_COLS;
+        const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
         for (int kb = 0; kb < wk.num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
@@ -169,16 +184,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int kcol = wk.a_col0 + kb * BK;
           const int krow = wk.b_row0 + kb * BK;
           if constexpr (CG == 1) {
-            ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pol);
-#pragma unroll
-            for (int j = 0; j < C::B_COLS / 64; ++j)
-              ptx::tma_load_2d(sb + j * (BK * 128), mbm, &full[stage], bcol + j * 64, krow, pol);
+            ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pa);
           } else {
-            ptx::tma_load_2d_cg2(sa, ma, &full[stage], kcol, arow, pol);
-#pragma unroll
-            for (int j = 0; j < C::B_COLS / 64; ++j)
-              ptx::tma_load_2d_cg2(sb + j * (BK * 128), mbm, &full[stage], bcol + j * 64, krow, pol);
+            ptx::tma_load_2d_cg2(sa, ma, &full[stage], kcol, arow, pa);
           }
+#pragma unroll
+          for (int j = 0; j < C::NACC; ++j)
+#pragma unroll
+            for (int s = 0; s < C::SUB_PER_ACC; ++s) {
+              uint8_t* dst = sb + (j * C::SUB_PER_ACC + s) * SUB_BYTES;
+              const int col = bcol + j * UMMA_N + s * 64;
+              if constexpr (CG == 1) ptx::tma_load_2d(dst, mbm, &full[stage], col, krow, pb);
+              else ptx::tma_load_2d_cg2(dst, mbm, &full[stage], col, krow, pb);
+            }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -186,36 +204,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread, leader CTA) =====================
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, BN, 0, 1);
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 1);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      // all MMAs of one k-block into accumulator `acc_col`
+      auto issue = [&](int stg, uint32_t acc_col, int j, bool first_kb) {
+        const uint32_t sa = ptx::smem_u32(smem_a + stg * C::A_BYTES);
+        const uint32_t sb = ptx::smem_u32(smem_b + stg * C::B_BYTES) + j * C::SUB_PER_ACC * SUB_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          // A: K-major SW128, 8-row groups 1024 B apart; advance 32 B per UMMA_K.
+          const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
+          // B: MN-major SW128; 64-column blocks SUB_BYTES apart (LBO), 8-k groups
+          // 1024 B apart (SBO); advance 16 k-rows = 2048 B per UMMA_K.
+          const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 128), SUB_BYTES, 1024);
+          ptx::umma_f16<CG>(tmem_base + acc_col, adesc, bdesc, idesc, (!first_kb || kk) ? 1u : 0u);
+        }
+      };
       for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
         const int w = find_work(works, nwork, t);
         const int num_kb = works[w].num_kb;
-        const int as = it & 1;
-        const uint32_t aphase = (it >> 1) & 1;
-        ptx::mbar_wait(&tmem_empty[as], aphase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+        const int buf = it % C::NBUF;
+        const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
+        if constexpr (C::NACC == 1) {
+          ptx::mbar_wait(&tmem_empty[buf], tph ^ 1);
           ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
-          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            // A: K-major SW128, 8-row groups 1024 B apart; advance 32 B per UMMA_K.
-            const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
-            // B: MN-major SW128; 64-column blocks BK*128 B apart (LBO), 8-k groups
-            // 1024 B apart (SBO); advance 16 k-rows = 2048 B per UMMA_K.
-            const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 128), BK * 128, 1024);
-            ptx::umma_f16<CG>(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            issue(stage, buf * UMMA_N, 0, kb == 0);
+            ptx::umma_commit<CG>(&empty[stage], 0x3);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::umma_commit<CG>(&empty[stage], 0x3);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        } else {
+          // accumulator 0 runs ahead by D k-blocks while the epilogue drains accumulator 1
+          const int D = min(C::STAGES - 1, num_kb);
+          ptx::mbar_wait(&tmem_empty[0], tph ^ 1);
+          ptx::tc_fence_after();
+          const int stage0 = stage;
+          for (int kb = 0; kb < D; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            issue(stage, 0, 0, kb == 0);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          ptx::mbar_wait(&tmem_empty[1], tph ^ 1);
+          ptx::tc_fence_after();
+          int st = stage0;
+          for (int kb = 0; kb < D; ++kb) {
+            issue(st, UMMA_N, 1, kb == 0);
+            ptx::umma_commit<CG>(&empty[st], 0x3);
+            if (++st == C::STAGES) st = 0;
+          }
+          for (int kb = D; kb < num_kb; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            issue(stage, 0, 0, false);
+            issue(stage, UMMA_N, 1, false);
+            ptx::umma_commit<CG>(&empty[stage], 0x3);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
         }
-        ptx::umma_commit<CG>(&tmem_full[as], 0x3);
+        ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
       }
     }
   } else {
@@ -224,72 +275,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t* ebuf = smem_epi + (warp - 2) * 2 * EPI_BOX_BYTES;
     const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
     int it = 0;
-    int buf = 0;
+    int sbuf = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
       const int w = find_work(works, nwork, t);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
       int mb, nb;
       tile_coords(wk, t - wk.tile_start, mb, nb);
-      const int as = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      ptx::mbar_wait(&tmem_full[as], aphase);
+      const int buf = it % C::NBUF;
+      const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
+      ptx::mbar_wait(&tmem_full[buf], tph);
       ptx::tc_fence_after();
       const int row_in_op = mb * BM * CG + (int)cta_rank * BM + q * 32;   // first row of this warp
-      const int col_in_op = nb * BN;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + ch * 32, r);
-        ptx::tmem_ld_wait();
-        if (ch == BN / 32 - 1) {
-          // accumulator fully drained into registers: hand TMEM back to the MMA warp
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (CG == 1) ptx::mbar_arrive(&tmem_empty[as]);
-            else ptx::mbar_arrive_cluster(&tmem_empty[as], 0);
+      for (int j = 0; j < C::NACC; ++j) {
+        const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * UMMA_N;
+        const int col_acc = nb * NT + j * UMMA_N;
+#pragma unroll 1
+        for (int ch = 0; ch < UMMA_N / 32; ++ch) {
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc_col + ch * 32, r);
+          ptx::tmem_ld_wait();
+          if (ch == UMMA_N / 32 - 1) {
+            // accumulator drained into registers: hand it back to the MMA warp
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              uint64_t* bar = &tmem_empty[C::NACC == 1 ? buf : j];
+              if constexpr (CG == 1) ptx::mbar_arrive(bar);
+              else ptx::mbar_arrive_cluster(bar, 0);
+            }
           }
-        }
-        if (wk.c_remote == 3) {
-          // (profiling only) accumulator dropped: isolates the main loop's cost
-        } else if (wk.c_remote != 1) {
-          // registers -> swizzled smem box -> TMA reduce-add into C
-          if (lane == 0) ptx::bulk_wait_read<1>();
-          __syncwarp();
-          const uint32_t base = ebuf_u32 + buf * EPI_BOX_BYTES + lane * 128;
+          const int col0 = col_acc + ch * 32;
+          if (wk.c_remote == 3) {
+            // (profiling only) accumulator dropped: isolates the main loop's cost
+          } else if (wk.c_remote != 1) {
+            // registers -> swizzled smem box -> TMA reduce-add into C
+            if (lane == 0) ptx::bulk_wait_read<1>();
+            __syncwarp();
+            const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES + lane * 128;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t addr = base + ((j ^ (lane & 7)) << 4);
-            ptx::st_shared_v4(addr, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          }
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
-              ptx::tma_store_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
-                                wk.c_row0 + row_in_op);
-            else
-              ptx::tma_reduce_add_2d(mc, ebuf + buf * EPI_BOX_BYTES, wk.c_col0 + col_in_op + ch * 32,
-                                     wk.c_row0 + row_in_op);
-            ptx::bulk_commit();
-          }
-          buf ^= 1;
-        } else {
-          // fused remote accumulate: red.global.add into the (peer) C tile
-          const int row = row_in_op + lane;
-          const int col0 = col_in_op + ch * 32;
-          if (row < wk.m) {
-            float* rowp = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0;
-            if (wk.c_vec_ok && col0 + 32 <= wk.n) {
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t addr = base + ((i ^ (lane & 7)) << 4);
+              ptx::st_shared_v4(addr, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
+                ptx::tma_store_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+              else
+                ptx::tma_reduce_add_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+              ptx::bulk_commit();
+            }
+            sbuf ^= 1;
+          } else {
+            // fused remote accumulate: red.global.add into the (peer) C tile
+            const int row = row_in_op + lane;
+            if (row < wk.m && col0 < wk.n) {
+              float* rowp = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0;
+              if (wk.c_vec_ok && col0 + 32 <= wk.n) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                ptx::red_add_v4_f32(rowp + col0 + 4 * j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            } else {
+                for (int i = 0; i < 8; ++i)
+                  ptx::red_add_v4_f32(rowp + col0 + 4 * i, __uint_as_float(r[4 * i]),
+                                      __uint_as_float(r[4 * i + 1]), __uint_as_float(r[4 * i + 2]),
+                                      __uint_as_float(r[4 * i + 3]));
+              } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col0 + j < wk.n) ptx::red_add_f32(rowp + col0 + j, __uint_as_float(r[j]));
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < wk.n) ptx::red_add_f32(rowp + col0 + i, __uint_as_float(r[i]));
+              }
             }
           }
         }
@@ -341,36 +396,39 @@ static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint
   return UM_OK;
 }
 
-static int raster_group() {
-  static int g = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* e = getenv("UM_GEMM_GROUP");
-    g = e ? atoi(e) : GROUP_M;
-    if (g == 0) g = GROUP_M;
-  });
-  return g;
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
 }
 
-static int g_cta_group = 2;  // default kernel variant; UM_GEMM_CG=1 env selects the 1-CTA kernel
-
-static int cta_group() {
+// Tuning knobs (read once): UM_GEMM_CG=1|2, UM_GEMM_NT=256|512 (0 = auto),
+// UM_GEMM_GROUP=<m-tiles, negative: n-tiles>, UM_GEMM_APOL / UM_GEMM_BPOL
+// = 0 normal | 1 evict_first | 2 evict_last (-1 = auto).
+struct Knobs {
+  int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1;
+};
+static const Knobs& knobs() {
+  static Knobs k;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* e = getenv("UM_GEMM_CG");
-    if (e && e[0] == '1') g_cta_group = 1;
+    k.cg = env_int("UM_GEMM_CG", 2) == 1 ? 1 : 2;
+    k.nt = env_int("UM_GEMM_NT", 0);
+    k.group = env_int("UM_GEMM_GROUP", GROUP_M);
+    if (k.group == 0) k.group = GROUP_M;
+    k.apol = env_int("UM_GEMM_APOL", -1);
+    k.bpol = env_int("UM_GEMM_BPOL", -1);
   });
-  return g_cta_group;
+  return k;
 }
 
-template <int CG>
+template <int CG, int NT>
 static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int total_tiles, int device,
                   cudaStream_t stream) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, NT>;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
   if (!attr_set[device]) {
-    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES));
     attr_set[device] = true;
   }
@@ -389,15 +447,16 @@ static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG>, d_works, d_maps, nwork, total_tiles));
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, d_works, d_maps, nwork, total_tiles));
   return UM_OK;
 }
 
 // TMA requires the innermost start coordinate of a box to be 16-byte aligned
 // (measured: an unaligned column offset raises an illegal-instruction fault;
-// row offsets are free), and a 16-byte aligned base and row pitch.  Slices of misaligned partitionings (e.g. 3x4 tiles,
-// cli.py:151-152) therefore get their A/B slice staged into an aligned scratch
-// and their C update routed through the pointer-based red.global epilogue.
+// row offsets are free), and a 16-byte aligned base and row pitch.  Slices of
+// misaligned partitionings (e.g. 3x4 tiles, cli.py:151-152) therefore get
+// their A/B slice staged into an aligned scratch and their C update routed
+// through the pointer-based red.global epilogue.
 static inline bool inner_aligned(const um_view& v) {
   const int64_t es = esize(v.dtype);
   return (v.col_lo * es) % 16 == 0 && (v.pitch * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(v.base) & 15) == 0;
@@ -407,8 +466,28 @@ static inline int64_t aligned_pitch(int64_t cols, int32_t dtype) {
   return (cols + per16 - 1) / per16 * per16;
 }
 
+// Pick the kernel variant for a launch: 256x512 pair tiles when there is
+// enough work for at least two waves of them, else 256x256 (or 128x256).
+static void pick_variant(const std::vector<um_gemm_op>& ops, int sms, int& cg, int& nt) {
+  const Knobs& kn = knobs();
+  cg = kn.cg;
+  if (cg == 1) {
+    nt = 256;
+    return;
+  }
+  if (kn.nt == 256 || kn.nt == 512) {
+    nt = kn.nt;
+    return;
+  }
+  int64_t tiles512 = 0;
+  for (const auto& op : ops) {
+    const int64_t m = view_rows(op.a), n = view_cols(op.b);
+    if (m && n) tiles512 += ((m + 255) / 256) * ((n + 511) / 512);
+  }
+  nt = tiles512 >= 2 * (sms / 2) ? 512 : 256;
+}
+
 int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t stream) {
-  const int CG = cta_group();
   DeviceGuard guard(device);
   // ---- stage misaligned operand slices
   std::vector<um_gemm_op> ops(ops_in, ops_in + nops);
@@ -452,6 +531,13 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
       if (p) cudaFreeAsync(p, s);
     }
   } scratch_guard{scratch, stream};
+
+  int sms = 0;
+  UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int CG = 2, NT = 256;
+  pick_variant(ops, sms, CG, NT);
+  const Knobs& kn = knobs();
+
   std::vector<Work> works;
   std::vector<CUtensorMap> maps;
   works.reserve(nops);
@@ -481,7 +567,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.n = (int32_t)n;
     w.k = (int32_t)k;
     w.tiles_m = (int32_t)((m + BM * CG - 1) / (BM * CG));
-    w.tiles_n = (int32_t)((n + BN - 1) / BN);
+    w.tiles_n = (int32_t)((n + NT - 1) / NT);
     w.num_kb = (int32_t)((k + BK - 1) / BK);
     w.tile_start = total;
     w.c_remote = op.c_remote;
@@ -499,7 +585,14 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.c_col0 = (int32_t)op.c.col_lo;
     w.c_pitch = op.c.pitch;
     w.c_ptr = reinterpret_cast<float*>(op.c.base);
-    w.group = raster_group();
+    w.group = kn.group;
+    // L2 eviction hints default to normal: measured on the box, evict_last on
+    // the group-reused operand + evict_first on the streamed one lowered the
+    // sustained rate (1144 vs 1211 TFLOP/s at group 16); kept as knobs.
+    w.a_pol = kn.apol >= 0 ? kn.apol : 0;
+    w.b_pol = kn.bpol >= 0 ? kn.bpol : 0;
+    if (w.a_pol > 2) w.a_pol = 0;
+    if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
     total += w.tiles_m * w.tiles_n;
     CUtensorMap ma, mbm, mc;
@@ -526,8 +619,10 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
   UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
   const CUtensorMap* d_maps = reinterpret_cast<const CUtensorMap*>(dbuf);
   const Work* d_works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
-  int rc = (CG == 2) ? launch<2>(d_works, d_maps, (int)works.size(), total, device, stream)
-                     : launch<1>(d_works, d_maps, (int)works.size(), total, device, stream);
+  int rc;
+  if (CG == 1) rc = launch<1, 256>(d_works, d_maps, (int)works.size(), total, device, stream);
+  else if (NT == 512) rc = launch<2, 512>(d_works, d_maps, (int)works.size(), total, device, stream);
+  else rc = launch<2, 256>(d_works, d_maps, (int)works.size(), total, device, stream);
   cudaFreeAsync(dbuf, stream);
   return rc;
 }
@@ -551,11 +646,14 @@ extern "C" int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t de
 }
 
 extern "C" int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group) {
-  const int cg = um::gemm::cta_group();
+  const auto& kn = um::gemm::knobs();
+  const int cg = kn.cg;
+  const int nt = cg == 1 ? 256 : (kn.nt == 256 ? 256 : 512);
   if (bm) *bm = um::gemm::BM * cg;
-  if (bn) *bn = um::gemm::BN;
+  if (bn) *bn = nt;
   if (bk) *bk = um::gemm::BK;
-  if (stages) *stages = cg == 1 ? um::gemm::Cfg<1>::STAGES : um::gemm::Cfg<2>::STAGES;
+  if (stages) *stages = cg == 1 ? um::gemm::Cfg<1, 256>::STAGES
+                                : (nt == 512 ? um::gemm::Cfg<2, 512>::STAGES : um::gemm::Cfg<2, 256>::STAGES);
   if (cta_group) *cta_group = cg;
   return UM_OK;
 }
