@@ -29,8 +29,8 @@
 //  * epilogue: tcgen05.ld -> registers -> swizzled smem -> TMA reduce-add
 //    (cp.reduce.async.bulk.tensor ... add) into the local C tile, or
 //    red.global.add.v4.f32 straight into a peer C tile (fused K3).
-//  * L2: tiles are walked in groups of m-tiles; the operand reused across the
-//    group is loaded evict_last, the streamed one evict_first.
+//  * L2: tiles are walked in groups of m-tiles so a wave of clusters shares A
+//    and B panels; per-operand eviction hints are available as knobs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -84,6 +84,7 @@ struct alignas(16) Work {
   int32_t c_row0, c_col0;
   int32_t c_vec_ok, group;
   int32_t a_pol, b_pol;     // L2 policy: 0 normal, 1 evict_first, 2 evict_last
+  int32_t c_pol, prefetch;  // L2 policy of the C reduce-add (-1: no hint); L2 prefetch distance (k-blocks)
   int64_t c_pitch;
   float* c_ptr;
 };
@@ -176,7 +177,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tile_coords(wk, t - wk.tile_start, mb, nb);
         const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
+        // L2 prefetch `pf` k-blocks ahead of the loads: the smem ring only
+        // covers ~4 k-blocks of latency, the prefetch turns the rest into L2 hits
+        auto prefetch = [&](int kb) {
+          ptx::tma_prefetch_2d(ma, wk.a_col0 + kb * BK, arow);
+#pragma unroll
+          for (int j = 0; j < C::NACC; ++j)
+#pragma unroll
+            for (int s = 0; s < C::SUB_PER_ACC; ++s)
+              ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, wk.b_row0 + kb * BK);
+        };
+        const int pf = wk.prefetch;
+        for (int kb = 0; kb < min(pf, wk.num_kb); ++kb) prefetch(kb);
         for (int kb = 0; kb < wk.num_kb; ++kb) {
+          if (pf > 0 && kb + pf < wk.num_kb) prefetch(kb + pf);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
@@ -272,6 +286,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ===================== Epilogue (4 warps) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint64_t cpols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
+    uint64_t cpol = cpols[0];
     uint8_t* ebuf = smem_epi + (warp - 2) * 2 * EPI_BOX_BYTES;
     const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
     int it = 0;
@@ -280,6 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int w = find_work(works, nwork, t);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
+      if (wk.c_pol >= 0) cpol = cpols[wk.c_pol];
       int mb, nb;
       tile_coords(wk, t - wk.tile_start, mb, nb);
       const int buf = it % C::NBUF;
@@ -324,6 +341,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) {
               if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
                 ptx::tma_store_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+              else if (wk.c_pol >= 0)
+                ptx::tma_reduce_add_2d_hint(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op,
+                                            cpol);
               else
                 ptx::tma_reduce_add_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
               ptx::bulk_commit();
@@ -380,6 +400,23 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+// L2 sector promotion of TMA loads: UM_GEMM_PROMO = 0 none | 1 64B | 2 128B | 3 256B (default 256B)
+static CUtensorMapL2promotion l2_promotion() {
+  static int p = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("UM_GEMM_PROMO");
+    p = (e && *e) ? atoi(e) : 3;
+    if (p < 0 || p > 3) p = 3;
+  });
+  switch (p) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint32_t box_rows, const char* what) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return fail(UM_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
@@ -389,7 +426,7 @@ static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, v.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(UM_ECUDA, std::string("cuTensorMapEncodeTiled failed for ") + what + " (code " +
                               std::to_string((int)r) + ")");
@@ -405,7 +442,7 @@ static int env_int(const char* name, int dflt) {
 // UM_GEMM_GROUP=<m-tiles, negative: n-tiles>, UM_GEMM_APOL / UM_GEMM_BPOL
 // = 0 normal | 1 evict_first | 2 evict_last (-1 = auto).
 struct Knobs {
-  int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1;
+  int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 4;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -417,6 +454,8 @@ static const Knobs& knobs() {
     if (k.group == 0) k.group = GROUP_M;
     k.apol = env_int("UM_GEMM_APOL", -1);
     k.bpol = env_int("UM_GEMM_BPOL", -1);
+    k.cpol = env_int("UM_GEMM_CPOL", -1);
+    k.prefetch = std::max(0, env_int("UM_GEMM_PF", 4));
   });
   return k;
 }
@@ -591,6 +630,8 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     // sustained rate (1144 vs 1211 TFLOP/s at group 16); kept as knobs.
     w.a_pol = kn.apol >= 0 ? kn.apol : 0;
     w.b_pol = kn.bpol >= 0 ? kn.bpol : 0;
+    w.c_pol = kn.cpol >= 0 && kn.cpol <= 2 ? kn.cpol : -1;
+    w.prefetch = kn.prefetch;
     if (w.a_pol > 2) w.a_pol = 0;
     if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);

@@ -112,6 +112,11 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// Warm L2 with a box ahead of its load (no smem, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1)
+               : "memory");
+}
 // 2D tiled reduce-add shared -> global (fp32 add performed at L2).
 __device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -123,6 +128,14 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
                "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
                : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d_hint(const void* tmap, const void* smem_src, int32_t c0, int32_t c1,
+                                                       uint64_t policy) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::
+          "l"(tmap),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>

@@ -88,6 +88,7 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
     _copy_rows(B, b_host, 0, k, lambda d: h2d[d], True, up)
     b_events = [e for evs in up.values() for e in evs]
     full_ops = {r: rt.rotated_ops(A, B, C, cfg, r) for r in fab.local_ranks()}
+    cross = rt._cross_process(A, B, C, cfg)
     results = {r: rt.RunStats() for r in fab.local_ranks()}
     bounds = [m * i // panels for i in range(panels + 1)]
     done_all = []
@@ -98,7 +99,7 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
         up = {}
         _copy_rows(A, a_host, r0, r1, lambda d: h2d[d], True, up)
         ready = b_events + [e for evs in up.values() for e in evs]
-        if fab.world.size > 1:
+        if cross:
             fab.synchronize()            # remote ranks may pull these rows
         runs = []
         for r in fab.local_ranks():
@@ -117,7 +118,7 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
             st.launches += run.stats.launches
             st.gets += run.stats.gets
             st.staged_bytes += run.stats.staged_bytes
-        if fab.world.size > 1:
+        if cross:
             fab.synchronize()
         if C.c > 1:
             done = rt.reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done, rows=(r0, r1))

@@ -213,9 +213,18 @@ def rotated_ops(A, B, C, cfg: ExecConfig, caller: int) -> list:
 def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None) -> DirectSchedule:
     """Rotated op list + fetch-once staging plan (host-side, no device work).
 
-    `ops` overrides the planner's list (e.g. ops restricted to a row panel)."""
+    `ops` overrides the planner's list (e.g. ops restricted to a row panel).
+    Schedules of the planner's own list are cached per (matrices, knobs, rank):
+    placement is immutable, so repeated multiplies skip the host work."""
     if ops is None:
-        ops = rotated_ops(A, B, C, cfg, caller)
+        key = (id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets, caller)
+        cache = A.__dict__.setdefault("_sched_cache", {})
+        hit = cache.get(key)
+        if hit is not None and hit[0] is B and hit[1] is C:
+            return hit[2]
+        sched = lower_direct(A, B, C, cfg, caller, rotated_ops(A, B, C, cfg, caller))
+        cache[key] = (B, C, sched)
+        return sched
     fabric = A.fabric
     fetches: list[_Fetch] = []
     index: dict = {}
@@ -630,6 +639,38 @@ def run_ir(prog, graph, A, B, C, cfg: ExecConfig, caller: int) -> RunStats:
 # whole-multiply driver (runtime.py:339-387)
 # ---------------------------------------------------------------------------
 
+def _cross_process(A, B, C, cfg: ExecConfig) -> bool:
+    """Does any rank's schedule touch memory hosted by another process?
+
+    Decided from the plans of ALL ranks (identical on every process), so every
+    process takes the same barrier decision.  When nothing crosses a process
+    boundary (e.g. cfg2: A/C row blocks, B replicated) the multiply runs with
+    no host synchronisation at all.
+    """
+    fab = A.fabric
+    if fab.world.size == 1:
+        return False
+    key = ("cross", id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets)
+    cache = A.__dict__.setdefault("_sched_cache", {})
+    if key in cache:
+        return cache[key]
+    proc = fab.process_of
+    cross = False
+    for r in range(fab.nprocs):
+        sched = lower_direct(A, B, C, cfg, r)
+        if any(proc(f.owner) != proc(r) for f in sched.fetches):
+            cross = True
+        for i, op in enumerate(sched.ops):
+            if sched.c_remote[i] and proc(C.owner_rank(op.c_tile, C.replica_of(r))) != proc(r):
+                cross = True
+    if C.c > 1:
+        for t in C.grid.tiles():
+            if len({proc(C.owner_rank(t, rep)) for rep in range(C.c)}) > 1:
+                cross = True
+    cache[key] = cross
+    return cross
+
+
 def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                      execution: str = "direct", machine=None, max_compute: int | None = None,
                      max_comm: int | None = None, threaded: bool = False) -> dict[int, RunStats]:
@@ -646,6 +687,9 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
     fab.heap.exchange()
     ranks = fab.local_ranks()
     results: dict[int, RunStats] = {}
+    cross = _cross_process(A, B, C, cfg) if execution == "direct" else fab.world.size > 1
+    if cross:
+        fab.synchronize()            # owners' pending writes visible before any remote pull
     start = _current_events(fab)
     done = []
     if execution == "direct":
@@ -671,7 +715,7 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
                 prog = lowering.lower_exhaustive(g, machine, max_compute, max_comm)
             results[r] = run_ir(prog, g, A, B, C, cfg, r)
         done = _current_events(fab)
-    if fab.world.size > 1:
+    if cross:
         fab.synchronize()            # run-level barrier across processes
     if C.c > 1:
         reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done)
