@@ -109,6 +109,13 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def blas_threads(n: int):
+    """Use all n host threads in BLAS even under torchrun (which sets OMP_NUM_THREADS=1)."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=n, user_api="blas")
+
+
 def cpu_oracle_rate(m, n, k, p, desc, target_s: float):
     """Time the CPU oracle port (numpy fp64, all host threads) on a row sample.
 
@@ -118,8 +125,6 @@ def cpu_oracle_rate(m, n, k, p, desc, target_s: float):
     from oracle import um_oracle as O
 
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    rows = 64
     rng = np.random.default_rng(0)
 
     def run(rows):
@@ -131,9 +136,12 @@ def cpu_oracle_rate(m, n, k, p, desc, target_s: float):
         O.execute("c", *mats, a, b)
         return time.perf_counter() - t0
 
-    dt = run(rows)
-    rows = int(min(m, max(64, rows * target_s / max(dt, 1e-3))))
-    dt = run(rows)
+    with blas_threads(cores):
+        run(64)                                   # BLAS thread-pool warm-up
+        rows = 256
+        dt = run(rows)
+        rows = int(min(m, max(64, rows * target_s / max(dt, 1e-3))))
+        dt = run(rows)
     flops = 2.0 * rows * n * k
     return flops / dt / 1e12, f"{rows}x{n}x{k} row sample of {desc} (fp64 numpy oracle port)", cores, dt
 
@@ -156,12 +164,13 @@ def reference_arm(args):
     b = rng.uniform(-1, 1, size=(k, n))
     mats = [O.Mat("A", rows, k, O.Spec(rows, k, 1, 1), 1, 1), O.Mat("B", k, n, O.Spec(k, n, 1, 1), 1, 1),
             O.Mat("C", rows, n, O.Spec(rows, n, 1, 1), 1, 1)]
-    for _ in range(args.warmup):
-        O.execute("c", *mats, a, b)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.execute("c", *mats, a, b)
-    dt = (time.perf_counter() - t0) / args.steps
+    with blas_threads(cores):
+        for _ in range(args.warmup):
+            O.execute("c", *mats, a, b)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            O.execute("c", *mats, a, b)
+        dt = (time.perf_counter() - t0) / args.steps
     val = 2.0 * rows * n * k / dt / 1e12
     out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",

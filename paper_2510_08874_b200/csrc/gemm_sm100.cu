@@ -54,7 +54,7 @@ constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
-constexpr int GROUP_M = 32;   // default rasterisation group (m-tiles); UM_GEMM_GROUP overrides
+constexpr int GROUP_M = 16;   // default rasterisation group (m-tiles); UM_GEMM_GROUP overrides
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
 
@@ -85,6 +85,7 @@ struct alignas(16) Work {
   int32_t c_vec_ok, group;
   int32_t a_pol, b_pol;     // L2 policy: 0 normal, 1 evict_first, 2 evict_last
   int32_t c_pol, prefetch;  // L2 policy of the C reduce-add (-1: no hint); L2 prefetch distance (k-blocks)
+  int32_t sched_static, pad2;  // 1: static round-robin tiles (profiling A/B only)
   int64_t c_pitch;
   float* c_ptr;
 };
@@ -120,10 +121,19 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
   }
 }
 
+// Dynamic tile scheduling: the leader producer of each cluster takes the next
+// tile index from a global atomic counter and broadcasts it through a small
+// ring in shared memory (written into both CTAs of the pair) to every role.
+// Concurrently running tiles are therefore always a sliding window of
+// consecutive raster tiles, so tiles that share an operand panel run close in
+// time and reuse it from L2 (a static persistent schedule lets clusters drift
+// apart by whole tiles and the panels get re-read from DRAM).
+constexpr int TQ = 4;  // tile-queue depth (producer runs <= 3 tiles ahead of the epilogue)
+
 template <int CG, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_kernel(const Work* __restrict__ works, const CUtensorMap* __restrict__ maps, int nwork,
-                     int total_tiles) {
+                     int total_tiles, int* __restrict__ tile_counter) {
   using C = Cfg<CG, NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -136,13 +146,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tmem_full = bars + 2 * C::STAGES;       // [NBUF]
   uint64_t* tmem_empty = bars + 2 * C::STAGES + 2;  // [2]: per buffer (NACC=1) or per accumulator (NACC=2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint64_t* tq_full = bars + 2 * C::STAGES + 5;     // [TQ]
+  uint64_t* tq_empty = tq_full + TQ;                // [TQ] (leader CTA)
+  volatile int* tq = reinterpret_cast<volatile int*>(tq_empty + TQ);  // [TQ]
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t cta_rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
   const bool leader = cta_rank == 0;
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  constexpr int TQ_CONSUMERS = (CG == 2 ? 1 : 0) /*peer producer*/ + 1 /*MMA*/ + EPI_WARPS * CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -153,8 +165,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tmem_full[s], 1);
       ptx::mbar_init(&tmem_empty[s], EPI_WARPS * CG);
     }
+    for (int s = 0; s < TQ; ++s) {
+      ptx::mbar_init(&tq_full[s], 1);
+      ptx::mbar_init(&tq_empty[s], TQ_CONSUMERS);
+    }
     ptx::fence_mbar_init();
   }
+  // consumer side of the tile queue (one thread): i-th tile of this cluster
+  auto next_tile = [&](int i) -> int {
+    const int slot = i % TQ;
+    ptx::mbar_wait_cluster(&tq_full[slot], (uint32_t)(i / TQ) & 1u);
+    const int t = tq[slot];
+    if constexpr (CG == 1) ptx::mbar_arrive(&tq_empty[slot]);
+    else ptx::mbar_arrive_cluster(&tq_empty[slot], 0);
+    return t;
+  };
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
@@ -167,7 +192,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      for (int i = 0;; ++i) {
+        int t;
+        if (leader) {
+          // take the next tile and publish it to both CTAs of the pair
+          const int slot = i % TQ;
+          ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
+          t = works[0].sched_static ? (int)(blockIdx.x / CG) + i * (int)(gridDim.x / CG)  // A/B knob
+                                    : atomicAdd(tile_counter, 1);
+          if (t > total_tiles) t = total_tiles;
+          tq[slot] = t;
+          if constexpr (CG == 2) {
+            ptx::st_shared_cluster_u32((const void*)&tq[slot], 1, (uint32_t)t);
+            ptx::mbar_arrive_cluster(&tq_full[slot], 0);
+            ptx::mbar_arrive_cluster(&tq_full[slot], 1);
+          } else {
+            ptx::mbar_arrive_cluster(&tq_full[slot], 0);
+          }
+        } else {
+          t = next_tile(i);
+        }
+        if (t >= total_tiles) break;
         const int w = find_work(works, nwork, t);
         const Work& wk = works[w];
         const CUtensorMap* ma = &maps[3 * w + 0];
@@ -177,8 +222,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tile_coords(wk, t - wk.tile_start, mb, nb);
         const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
-        // L2 prefetch `pf` k-blocks ahead of the loads: the smem ring only
-        // covers ~4 k-blocks of latency, the prefetch turns the rest into L2 hits
+        // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
+        // default: measured slower, 1437 -> 1143..1292 TFLOP/s on cfg2)
         auto prefetch = [&](int kb) {
           ptx::tma_prefetch_2d(ma, wk.a_col0 + kb * BK, arow);
 #pragma unroll
@@ -236,7 +281,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::umma_f16<CG>(tmem_base + acc_col, adesc, bdesc, idesc, (!first_kb || kk) ? 1u : 0u);
         }
       };
-      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+      for (;; ++it) {
+        const int t = next_tile(it);
+        if (t >= total_tiles) break;
         const int w = find_work(works, nwork, t);
         const int num_kb = works[w].num_kb;
         const int buf = it % C::NBUF;
@@ -292,7 +339,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
     int it = 0;
     int sbuf = 0;
-    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+    for (;; ++it) {
+      int t = 0;
+      if (lane == 0) t = next_tile(it);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= total_tiles) break;
       const int w = find_work(works, nwork, t);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
@@ -400,14 +451,15 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// L2 sector promotion of TMA loads: UM_GEMM_PROMO = 0 none | 1 64B | 2 128B | 3 256B (default 256B)
+// L2 sector promotion of TMA loads: UM_GEMM_PROMO = 0 none | 1 64B | 2 128B | 3 256B (default none:
+// measured 1459 vs 1427 TFLOP/s for 256B on cfg2, DRAM bytes unchanged)
 static CUtensorMapL2promotion l2_promotion() {
   static int p = -1;
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = getenv("UM_GEMM_PROMO");
-    p = (e && *e) ? atoi(e) : 3;
-    if (p < 0 || p > 3) p = 3;
+    p = (e && *e) ? atoi(e) : 0;
+    if (p < 0 || p > 3) p = 0;
   });
   switch (p) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
@@ -442,7 +494,7 @@ static int env_int(const char* name, int dflt) {
 // UM_GEMM_GROUP=<m-tiles, negative: n-tiles>, UM_GEMM_APOL / UM_GEMM_BPOL
 // = 0 normal | 1 evict_first | 2 evict_last (-1 = auto).
 struct Knobs {
-  int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 4;
+  int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 0, sched_static = 0;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -455,14 +507,15 @@ static const Knobs& knobs() {
     k.apol = env_int("UM_GEMM_APOL", -1);
     k.bpol = env_int("UM_GEMM_BPOL", -1);
     k.cpol = env_int("UM_GEMM_CPOL", -1);
-    k.prefetch = std::max(0, env_int("UM_GEMM_PF", 4));
+    k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
+    k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
   });
   return k;
 }
 
 template <int CG, int NT>
-static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int total_tiles, int device,
-                  cudaStream_t stream) {
+static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int total_tiles, int* d_counter,
+                  int device, cudaStream_t stream) {
   using C = Cfg<CG, NT>;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
@@ -486,7 +539,7 @@ static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, d_works, d_maps, nwork, total_tiles));
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, d_works, d_maps, nwork, total_tiles, d_counter));
   return UM_OK;
 }
 
@@ -632,6 +685,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.b_pol = kn.bpol >= 0 ? kn.bpol : 0;
     w.c_pol = kn.cpol >= 0 && kn.cpol <= 2 ? kn.cpol : -1;
     w.prefetch = kn.prefetch;
+    w.sched_static = kn.sched_static;
     if (w.a_pol > 2) w.a_pol = 0;
     if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
@@ -652,7 +706,8 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
   // One stream-ordered allocation carries the work list and the tensor maps.
   const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
   const size_t works_bytes = works.size() * sizeof(Work);
-  std::vector<uint8_t> host(maps_bytes + works_bytes);
+  // ... followed by the dynamic scheduler's tile counter (zeroed by the same copy)
+  std::vector<uint8_t> host(maps_bytes + works_bytes + 16, 0);
   memcpy(host.data(), maps.data(), maps_bytes);
   memcpy(host.data() + maps_bytes, works.data(), works_bytes);
   void* dbuf = nullptr;
@@ -660,10 +715,11 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
   UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
   const CUtensorMap* d_maps = reinterpret_cast<const CUtensorMap*>(dbuf);
   const Work* d_works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
+  int* d_counter = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes + works_bytes);
   int rc;
-  if (CG == 1) rc = launch<1, 256>(d_works, d_maps, (int)works.size(), total, device, stream);
-  else if (NT == 512) rc = launch<2, 512>(d_works, d_maps, (int)works.size(), total, device, stream);
-  else rc = launch<2, 256>(d_works, d_maps, (int)works.size(), total, device, stream);
+  if (CG == 1) rc = launch<1, 256>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
+  else if (NT == 512) rc = launch<2, 512>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
+  else rc = launch<2, 256>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
   cudaFreeAsync(dbuf, stream);
   return rc;
 }
