@@ -54,7 +54,10 @@ constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
-constexpr int GROUP_M = 16;   // default rasterisation group (m-tiles); UM_GEMM_GROUP overrides
+// default rasterisation group: 4 n-tiles (negative = group along n), i.e. a
+// 4-panel slice of B stays hot while A streams; measured best of {-4,4,8,16,32}
+// on cfg2 / 16384^3 / cfg3 shapes with the dynamic scheduler. UM_GEMM_GROUP overrides.
+constexpr int GROUP_M = -4;
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
 
@@ -318,7 +321,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::umma_commit<CG>(&empty[st], 0x3);
             if (++st == C::STAGES) st = 0;
           }
-          for (int kb = D; kb < num_kb; ++kb) {
+          // accumulator 0 also finishes E k-blocks early, so its drain overlaps
+          // accumulator 1's tail
+          const int E = min(C::STAGES - 1, num_kb - D);
+          for (int kb = D; kb < num_kb - E; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
             issue(stage, 0, 0, false);
@@ -326,8 +332,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::umma_commit<CG>(&empty[stage], 0x3);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
+          const int stageE = stage;
+          for (int kb = num_kb - E; kb < num_kb; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            issue(stage, 0, 0, false);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+          ptx::umma_commit<CG>(&tmem_full[0], 0x3);
+          st = stageE;
+          for (int kb = num_kb - E; kb < num_kb; ++kb) {
+            issue(st, UMMA_N, 1, false);
+            ptx::umma_commit<CG>(&empty[st], 0x3);
+            if (++st == C::STAGES) st = 0;
+          }
+          ptx::umma_commit<CG>(&tmem_full[1], 0x3);
         }
-        ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
+        if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
       }
     }
   } else {
@@ -352,11 +373,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(wk, t - wk.tile_start, mb, nb);
       const int buf = it % C::NBUF;
       const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
-      ptx::mbar_wait(&tmem_full[buf], tph);
-      ptx::tc_fence_after();
       const int row_in_op = mb * BM * CG + (int)cta_rank * BM + q * 32;   // first row of this warp
 #pragma unroll 1
       for (int j = 0; j < C::NACC; ++j) {
+        // NACC == 1: one barrier per TMEM buffer; NACC == 2: one per accumulator
+        ptx::mbar_wait(&tmem_full[C::NACC == 1 ? buf : j], tph);
+        ptx::tc_fence_after();
         const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * UMMA_N;
         const int col_acc = nb * NT + j * UMMA_N;
 #pragma unroll 1

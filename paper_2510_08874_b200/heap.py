@@ -166,6 +166,7 @@ class SymmetricHeap:
         self._cursor: dict[int, int] = {q: 0 for q in range(self.world.size)}
         self._unresolved: list = []
         self._owner_box = None
+        self._dirty = False   # chunks appended since the last exchange (same on every process)
 
     # -- allocation -------------------------------------------------------------------
 
@@ -189,6 +190,7 @@ class SymmetricHeap:
             size = self.first_chunk if not chunks else min(MAX_CHUNK, 2 * chunks[-1].size)
             size = max(size, _align(nbytes, 2 << 20))
             chunks.append(_Chunk(process, len(chunks), size, owned=process == self.world.rank))
+            self._dirty = True
             self._cursor[process] = 0
             if process == self.world.rank:
                 self._materialise(chunks[-1])
@@ -222,9 +224,13 @@ class SymmetricHeap:
     # -- multi-process publication ---------------------------------------------------------
 
     def exchange(self):
-        """Collective: publish own chunk handles, map every peer chunk, resolve segments."""
-        if self.world.size == 1:
+        """Collective: publish own chunk handles, map every peer chunk, resolve segments.
+
+        A no-op unless chunks were added since the last call; every process
+        replays the same allocation sequence, so all take the same branch."""
+        if self.world.size == 1 or not self._dirty:
             return
+        self._dirty = False
         mine = {ch.index: self.api.ipc_handle(ch.base) for ch in self._chunks[self.world.rank]
                 if ch.owned}
         all_handles = self.world.all_gather_object(mine)
