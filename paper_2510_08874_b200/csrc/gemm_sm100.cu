@@ -88,7 +88,7 @@ struct alignas(16) Work {
   int32_t c_vec_ok, group;
   int32_t a_pol, b_pol;     // L2 policy: 0 normal, 1 evict_first, 2 evict_last
   int32_t c_pol, prefetch;  // L2 policy of the C reduce-add (-1: no hint); L2 prefetch distance (k-blocks)
-  int32_t sched_static, pad2;  // 1: static round-robin tiles (profiling A/B only)
+  int32_t sched_static, no_end_stagger;  // profiling A/B knobs: static round-robin tiles; no end stagger
   int64_t c_pitch;
   float* c_ptr;
 };
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           // accumulator 0 also finishes E k-blocks early, so its drain overlaps
           // accumulator 1's tail
-          const int E = min(C::STAGES - 1, num_kb - D);
+          const int E = works[0].no_end_stagger ? 0 : min(C::STAGES - 1, num_kb - D);
           for (int kb = D; kb < num_kb - E; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
@@ -708,6 +708,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.c_pol = kn.cpol >= 0 && kn.cpol <= 2 ? kn.cpol : -1;
     w.prefetch = kn.prefetch;
     w.sched_static = kn.sched_static;
+    w.no_end_stagger = env_int("UM_GEMM_NO_END_STAGGER", 0) ? 1 : 0;
     if (w.a_pol > 2) w.a_pol = 0;
     if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
