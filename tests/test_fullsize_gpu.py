@@ -1,0 +1,86 @@
+"""Parity at BASELINE.json's FULL sizes (cfg2..cfg5), p = 1 and p = 8 ranks.
+
+At these sizes the oracle cannot recompute all of C, so two size-independent
+properties are checked on integer-valued synthetic inputs (exact in bf16,
+every fp32 partial sum < 2**24, so the product is exact):
+
+* sampled entries: 48 x 48 entries of C (replica 0) against the oracle,
+  computed from the counter-based fill restated in oracle/um_oracle.py
+  (rows of A and columns of B regenerated on the CPU);
+* checksum of checksums: sum_ij C_ij == sum_k (sum_i A_ik)(sum_j B_kj),
+  exact in fp64 (|total| < 2**53), so every element of C is covered.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import um_oracle as O
+from paper_2510_08874_b200 import ExecConfig, Stationarity, execute_multiply
+from paper_2510_08874_b200.cli import build_problem
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    # name: (m, n, k, a_part, b_part, c_part, c_a, c_b, c_c)  (c as a function of p)
+    "cfg2": (65536, 8192, 8192, "row", "2d", "row", lambda p: 1, lambda p: p, lambda p: 1),
+    "cfg3": (8192, 8192, 65536, "col", "row", "2d", lambda p: 1, lambda p: 1, lambda p: p),
+    "cfg4": (16384, 16384, 16384, "2d", "2d", "2d", lambda p: min(2, p), lambda p: min(2, p), lambda p: min(2, p)),
+    "cfg5": (16384, 16384, 16384, "2d", "col", "row", lambda p: 1, lambda p: 1, lambda p: 1),
+}
+SEED = 77
+
+
+def _col_sums(M) -> torch.Tensor:
+    """sum over rows of a matrix, fp64, from replica 0's device tiles."""
+    out = torch.zeros(M.global_shape.cols, dtype=torch.float64, device="cuda")
+    for t in M.grid.tiles():
+        b = M.tile_bounds(t)
+        out[b.cols.lo:b.cols.hi] += M.segment(t, 0).view2d().double().sum(0)
+    return out
+
+
+def _row_sums(M) -> torch.Tensor:
+    out = torch.zeros(M.global_shape.rows, dtype=torch.float64, device="cuda")
+    for t in M.grid.tiles():
+        b = M.tile_bounds(t)
+        out[b.rows.lo:b.rows.hi] += M.segment(t, 0).view2d().double().sum(1)
+    return out
+
+
+def _total(M) -> float:
+    return float(sum(M.segment(t, 0).view2d().double().sum().item() for t in M.grid.tiles()))
+
+
+def _entries(M, rows, cols) -> np.ndarray:
+    out = np.zeros((len(rows), len(cols)))
+    for t in M.grid.tiles():
+        b = M.tile_bounds(t)
+        ri = [i for i, r in enumerate(rows) if b.rows.lo <= r < b.rows.hi]
+        ci = [j for j, c in enumerate(cols) if b.cols.lo <= c < b.cols.hi]
+        if not ri or not ci:
+            continue
+        v = M.segment(t, 0).view2d()
+        rr = torch.tensor([rows[i] - b.rows.lo for i in ri], device="cuda")
+        cc = torch.tensor([cols[j] - b.cols.lo for j in ci], device="cuda")
+        out[np.ix_(ri, ci)] = v[rr][:, cc].double().cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("p", [1, 8])
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_fullsize_exact(cuda, name, p):
+    m, n, k, ap, bp, cp, fa, fb, fc = CONFIGS[name]
+    fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, fa(p), fb(p), fc(p), seed=SEED, synthetic=True)
+    execute_multiply(A, B, C, ExecConfig(stationarity=Stationarity.STATIONARY_C))
+    torch.cuda.synchronize()
+    # sampled entries vs the oracle (fill restated on the CPU)
+    rng = np.random.default_rng(sum(map(ord, name)) * 10 + p)
+    rows = sorted(set(rng.integers(0, m, 46).tolist()) | {0, m - 1})
+    cols = sorted(set(rng.integers(0, n, 46).tolist()) | {0, n - 1})
+    a_rows = np.concatenate([O.fill_values(SEED, r, r + 1, 0, k, "int") for r in rows]).astype(np.float64)
+    b_cols = np.concatenate([O.fill_values(SEED + 1, 0, k, c, c + 1, "int") for c in cols], axis=1).astype(np.float64)
+    assert np.array_equal(_entries(C, rows, cols), a_rows @ b_cols), (name, p)
+    # checksum of checksums over all of C
+    expect = float(torch.dot(_col_sums(A), _row_sums(B)).item())
+    assert _total(C) == expect, (name, p)
