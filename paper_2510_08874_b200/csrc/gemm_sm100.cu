@@ -133,11 +133,28 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
 // apart by whole tiles and the panels get re-read from DRAM).
 constexpr int TQ = 4;  // tile-queue depth (producer runs <= 3 tiles ahead of the epilogue)
 
+constexpr int MAX_INLINE_OPS = 8;
+struct alignas(64) LaunchArgs {
+  const Work* works;          // null: use inl_works
+  const CUtensorMap* maps;    // null: use inl_maps
+  int nwork, total_tiles;
+  int* counters;              // per-stream {tile, done}; left zeroed by the kernel
+  CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
+  Work inl_works[MAX_INLINE_OPS];
+};
+static_assert(sizeof(LaunchArgs) <= 4096, "kernel parameter block");
+
 template <int CG, int NT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_bf16_kernel(const Work* __restrict__ works, const CUtensorMap* __restrict__ maps, int nwork,
-                     int total_tiles, int* __restrict__ tile_counter) {
+    gemm_bf16_kernel(const __grid_constant__ LaunchArgs args) {
   using C = Cfg<CG, NT>;
+  // small op lists travel inside the kernel parameters (no per-launch device
+  // allocation or host->device copy); larger ones in a global-memory block
+  const Work* __restrict__ works = args.works ? args.works : args.inl_works;
+  const CUtensorMap* __restrict__ maps = args.maps ? args.maps : args.inl_maps;
+  const int nwork = args.nwork;
+  const int total_tiles = args.total_tiles;
+  int* const tile_counter = args.counters;       // [0] next tile, [1] finished clusters
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -215,7 +232,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
           t = next_tile(i);
         }
-        if (t >= total_tiles) break;
+        if (t >= total_tiles) {
+          if (leader) {
+            // this cluster is done with the counter; the last one out re-zeroes
+            // it for the next launch on this stream
+            __threadfence();
+            if (atomicAdd(&tile_counter[1], 1) == (int)(gridDim.x / CG) - 1) {
+              atomicExch(&tile_counter[0], 0);
+              atomicExch(&tile_counter[1], 0);
+            }
+          }
+          break;
+        }
         const int w = find_work(works, nwork, t);
         const Work& wk = works[w];
         const CUtensorMap* ma = &maps[3 * w + 0];
@@ -423,22 +451,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             sbuf ^= 1;
           } else {
-            // fused remote accumulate: red.global.add into the (peer) C tile
-            const int row = row_in_op + lane;
-            if (row < wk.m && col0 < wk.n) {
-              float* rowp = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0;
-              if (wk.c_vec_ok && col0 + 32 <= wk.n) {
+            // fused remote accumulate (K3): red.global.add into the (peer) C tile.
+            // The 32x32 chunk is transposed through swizzled smem so that each
+            // warp-wide red.v4 covers 4 full 128-byte row segments (coalesced
+            // over NVLink / into L2); no async buffer to wait for.
+            const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES;
+            __syncwarp();
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  ptx::red_add_v4_f32(rowp + col0 + 4 * i, __uint_as_float(r[4 * i]),
-                                      __uint_as_float(r[4 * i + 1]), __uint_as_float(r[4 * i + 2]),
-                                      __uint_as_float(r[4 * i + 3]));
-              } else {
+            for (int i = 0; i < 8; ++i)
+              ptx::st_shared_v4(base + lane * 128 + ((i ^ (lane & 7)) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                                r[4 * i + 3]);
+            __syncwarp();
+            const int c4 = lane & 7;          // 16-byte column group of this lane
+            const int col = col0 + 4 * c4;
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (col0 + i < wk.n) ptx::red_add_f32(rowp + col0 + i, __uint_as_float(r[i]));
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + (lane >> 3);   // row within the warp's 32
+              const int row = row_in_op + rr;
+              float4 v = ptx::ld_shared_v4f(base + rr * 128 + ((c4 ^ (rr & 7)) << 4));
+              if (row < wk.m && col < wk.n) {
+                float* dst = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0 + col;
+                if (wk.c_vec_ok && col + 4 <= wk.n) {
+                  ptx::red_add_v4_f32(dst, v.x, v.y, v.z, v.w);
+                } else {
+                  ptx::red_add_f32(dst, v.x);
+                  if (col + 1 < wk.n) ptx::red_add_f32(dst + 1, v.y);
+                  if (col + 2 < wk.n) ptx::red_add_f32(dst + 2, v.z);
+                  if (col + 3 < wk.n) ptx::red_add_f32(dst + 3, v.w);
+                }
               }
             }
+            sbuf ^= 1;
           }
         }
       }
@@ -535,10 +578,28 @@ static const Knobs& knobs() {
   return k;
 }
 
+// Per-(device, stream) scheduler counters {next tile, finished clusters}:
+// zeroed once at creation, re-zeroed by the last cluster of every launch, so
+// launches on one stream (serialised) reuse them with no per-launch memset.
+static int* stream_counters(int device, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, int*>> table;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : table)
+    if (e.first.first == device && e.first.second == stream) return e.second;
+  int* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  // zero in stream order: torch's streams are non-blocking, so a plain
+  // cudaMemset (legacy default stream) would race the first launch
+  if (cudaMemsetAsync(p, 0, 2 * sizeof(int), stream) != cudaSuccess) return nullptr;
+  table.push_back({{device, stream}, p});
+  return p;
+}
+
 template <int CG, int NT>
-static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int total_tiles, int* d_counter,
-                  int device, cudaStream_t stream) {
+static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   using C = Cfg<CG, NT>;
+  const int total_tiles = args.total_tiles;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
   if (!attr_set[device]) {
@@ -561,7 +622,7 @@ static int launch(const Work* d_works, const CUtensorMap* d_maps, int nwork, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, d_works, d_maps, nwork, total_tiles, d_counter));
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, args));
   return UM_OK;
 }
 
@@ -690,6 +751,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
       static const char* dbg = getenv("UM_GEMM_EPI_DEBUG");
       if (dbg && !strcmp(dbg, "store")) w.c_remote = 2;
       if (dbg && !strcmp(dbg, "none")) w.c_remote = 3;
+      if (dbg && !strcmp(dbg, "red")) w.c_remote = 1;  // coalesced red.global epilogue for local C
     }
     w.a_row0 = (int32_t)op.a.row_lo;
     w.a_col0 = (int32_t)op.a.col_lo;
@@ -726,24 +788,35 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     maps.push_back(mc);
   }
   if (works.empty()) return UM_OK;
-  // One stream-ordered allocation carries the work list and the tensor maps.
-  const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
-  const size_t works_bytes = works.size() * sizeof(Work);
-  // ... followed by the dynamic scheduler's tile counter (zeroed by the same copy)
-  std::vector<uint8_t> host(maps_bytes + works_bytes + 16, 0);
-  memcpy(host.data(), maps.data(), maps_bytes);
-  memcpy(host.data() + maps_bytes, works.data(), works_bytes);
+  static LaunchArgs args;  // host-side staging of the parameter block (calls for a device are serialised)
+  static std::mutex args_mu;
+  std::lock_guard<std::mutex> lock(args_mu);
+  memset(&args, 0, sizeof(args));
+  args.nwork = (int)works.size();
+  args.total_tiles = total;
+  args.counters = stream_counters(device, stream);
+  if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
   void* dbuf = nullptr;
-  UM_CUDA_CHECK(cudaMallocAsync(&dbuf, host.size(), stream));
-  UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
-  const CUtensorMap* d_maps = reinterpret_cast<const CUtensorMap*>(dbuf);
-  const Work* d_works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
-  int* d_counter = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes + works_bytes);
+  if (works.size() <= (size_t)MAX_INLINE_OPS) {
+    memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
+    memcpy(args.inl_works, works.data(), works.size() * sizeof(Work));
+  } else {
+    // large op lists: one stream-ordered allocation carries work list + tensor maps
+    const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
+    const size_t works_bytes = works.size() * sizeof(Work);
+    std::vector<uint8_t> host(maps_bytes + works_bytes);
+    memcpy(host.data(), maps.data(), maps_bytes);
+    memcpy(host.data() + maps_bytes, works.data(), works_bytes);
+    UM_CUDA_CHECK(cudaMallocAsync(&dbuf, host.size(), stream));
+    UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
+    args.maps = reinterpret_cast<const CUtensorMap*>(dbuf);
+    args.works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
+  }
   int rc;
-  if (CG == 1) rc = launch<1, 256>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
-  else if (NT == 512) rc = launch<2, 512>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
-  else rc = launch<2, 256>(d_works, d_maps, (int)works.size(), total, d_counter, device, stream);
-  cudaFreeAsync(dbuf, stream);
+  if (CG == 1) rc = launch<1, 256>(args, device, stream);
+  else if (NT == 512) rc = launch<2, 512>(args, device, stream);
+  else rc = launch<2, 256>(args, device, stream);
+  if (dbuf) cudaFreeAsync(dbuf, stream);
   return rc;
 }
 
