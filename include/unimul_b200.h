@@ -121,12 +121,36 @@ UM_API int um_most_square_grid(int64_t p, int64_t* gr, int64_t* gc);
 /* One component multiply C[c] += A[a] @ B[b] (bf16 in, fp32 accumulate).
  * c_remote = 0: epilogue TMA reduce-add into c (c on the launching device).
  * c_remote = 1: epilogue red.global.add straight into c (peer or IPC
- *               pointer) — the fused remote accumulate of fabric.py:203-234. */
+ *               pointer) — the fused remote accumulate of fabric.py:203-234.
+ * wait_flag != NULL: the op's operands are being delivered by a get (K2)
+ *               that signals *wait_flag = wait_value on arrival (um_signal);
+ *               the kernel's producer waits for it before loading this op's
+ *               tiles, so gets overlap the GEMMs of earlier ops inside ONE
+ *               launch — the ordering rule "a compute depends on its input
+ *               fetches" (runtime.py:233-236 PendingTileCopy.wait). */
 typedef struct {
   um_view a, b, c;
   int32_t c_remote;
-  int32_t reserved;
+  uint32_t wait_value;
+  const uint32_t* wait_flag;
+  int32_t a_get, b_get;    /* um_gemm_acc_fused: 1-based index of the get that delivers
+                              this op's a / b operand (0 = already resident)            */
 } um_gemm_op;
+
+/* A pull executed INSIDE the GEMM launch (um_gemm_acc_fused): src slice
+ * (local, peer or IPC-mapped) -> dst slice (a staging buffer on the launching
+ * device), same dtype and shape.  Replaces get_tile_async + PendingTileCopy
+ * (distmatrix.py:42-59,161-168 -> fabric.py:177-201) on the hot path.      */
+typedef struct {
+  um_view src, dst;
+} um_get_desc;
+
+/* Max pulls per fused launch. */
+#define UM_GEMM_MAX_GETS 64
+
+/* Ops per grouped launch that travel inside the kernel parameters; longer
+ * lists are staged through a stream-ordered device allocation.            */
+#define UM_GEMM_MAX_INLINE_OPS 40
 
 /* c += a @ b for a single op on `stream` (device = c.device unless remote). */
 UM_API int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, void* stream);
@@ -135,6 +159,16 @@ UM_API int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, voi
  * operands must be readable from `device`.  Equivalent to calling
  * um_gemm_acc for each op in order (accumulates commute).                  */
 UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream);
+
+/* Fused get -> GEMM: ONE persistent launch that pulls `gets` with dedicated
+ * get warps on every SM (chunks handed out in list order) while the tensor
+ * cores run the ops; an op whose a_get/b_get names a pull starts loading
+ * only after every chunk of that pull has landed (device-side acquire), so
+ * the reference's ordering rule "a compute depends on completion of its input
+ * fetches" (runtime.py:219-236) holds without host round trips.
+ * Deadlock-free: the get warps depend on nothing but their own loads.      */
+UM_API int um_gemm_acc_fused(const um_gemm_op* ops, int32_t nops, const um_get_desc* gets, int32_t ngets,
+                             int32_t device, void* stream);
 
 /* Tile/stage knobs of the GEMM (bench/profiling): returns 0 and fills.    */
 UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group);
@@ -148,6 +182,16 @@ UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages
  * copy engines of the launching stream's device (the paper's transport,
  * PAPER.md:69).                                                            */
 UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
+
+/* Arrival flag of a get: write `value` to the device word `flag` in stream
+ * order (after everything enqueued before it on `stream`), without using an
+ * SM (stream memory operation), so a running K1 launch waiting on the flag
+ * cannot starve it.  Replaces PendingTileCopy/PendingCopy.wait()
+ * (distmatrix.py:42-59, fabric.py:41-58) as the device-side completion signal.
+ * Returns UM_ECUDA if the device does not support stream memory operations. */
+UM_API int um_signal(uint32_t* flag, uint32_t value, void* stream);
+/* 1 if um_signal is usable on `device` (stream memory operations), else 0. */
+UM_API int um_signal_supported(int32_t device, int32_t* out);
 
 /* ======================================================================== */
 /* K3: one-sided accumulate (fabric.py:203-234, distmatrix.py:170-209)        */

@@ -26,6 +26,8 @@ UM_EVALUE = 5
 UM_ECUDA = 6
 UM_ECAPACITY = 7
 
+GEMM_MAX_INLINE_OPS = 40   # UM_GEMM_MAX_INLINE_OPS: ops per K1 launch carried in the kernel parameters
+GEMM_MAX_GETS = 64         # UM_GEMM_MAX_GETS: in-kernel pulls per fused launch
 UM_BF16 = 0
 UM_F32 = 1
 
@@ -65,7 +67,12 @@ class UmView(ctypes.Structure):
 
 class UmGemmOp(ctypes.Structure):
     _fields_ = [("a", UmView), ("b", UmView), ("c", UmView),
-                ("c_remote", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("c_remote", ctypes.c_int32), ("wait_value", ctypes.c_uint32),
+                ("wait_flag", ctypes.c_void_p), ("a_get", ctypes.c_int32), ("b_get", ctypes.c_int32)]
+
+
+class UmGetDesc(ctypes.Structure):
+    _fields_ = [("src", UmView), ("dst", UmView)]
 
 
 # Exported symbols and their C signatures (kept in sync with the header; the
@@ -80,8 +87,12 @@ _SIGS = {
     "um_most_square_grid": (ctypes.c_int, [ctypes.c_int64, _P(ctypes.c_int64), _P(ctypes.c_int64)]),
     "um_gemm_acc": (ctypes.c_int, [_P(UmView), _P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_gemm_acc_batch": (ctypes.c_int, [_P(UmGemmOp), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
+    "um_gemm_acc_fused": (ctypes.c_int, [_P(UmGemmOp), ctypes.c_int32, _P(UmGetDesc), ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_void_p]),
     "um_gemm_config": (ctypes.c_int, [_P(ctypes.c_int32)] * 5),
     "um_get": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
+    "um_signal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
+    "um_signal_supported": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_int32)]),
     "um_accumulate": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_void_p]),
     "um_copy": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),

@@ -73,26 +73,22 @@ static int current_device() {
 
 // ------------------------------------------------------------------ kernels
 
-// dst += src element-wise (fp32), dst possibly a peer pointer.  One block row
-// per (row, 4-column group); red.global.add keeps concurrent accumulates
-// atomic per element (fabric.py:226-227 takes a lock for the same guarantee).
+// dst += src element-wise (fp32), dst possibly a peer pointer.  2D grid (x:
+// 16-byte column groups, y: rows); red.global.add keeps concurrent
+// accumulates atomic per element (fabric.py:226-227 takes a lock for the same
+// guarantee).  Ragged tails (cols % 4) are handled by the vec == 0 variant.
 __global__ void accumulate_kernel(const float* __restrict__ src, int64_t src_pitch, float* dst, int64_t dst_pitch,
                                   int64_t rows, int64_t cols, int vec) {
   const int64_t groups = vec ? cols / 4 : cols;
-  const int64_t total = rows * groups;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / groups;
-    const int64_t g = i - r * groups;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     if (vec) {
       const float4 v = *reinterpret_cast<const float4*>(src + r * src_pitch + 4 * g);
       ptx::red_add_v4_f32(dst + r * dst_pitch + 4 * g, v.x, v.y, v.z, v.w);
     } else {
       ptx::red_add_f32(dst + r * dst_pitch + g, src[r * src_pitch + g]);
     }
-  }
-  if (vec && blockIdx.x == 0) {
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x)
-      for (int64_t c = groups * 4; c < cols; ++c) ptx::red_add_f32(dst + r * dst_pitch + c, src[r * src_pitch + c]);
   }
 }
 
@@ -104,29 +100,61 @@ struct SrcList {
 // dst += sum_i src_i, summed in list order into a register accumulator first
 // (the reference's acc, distmatrix.py:224-232).  Sources may be peer pointers
 // (P2P loads over NVLink); dst is written with plain stores (owner only).
+// HBM/NVLink-bound: a 2D grid (x: 16-byte column groups, U per thread, warp-
+// coalesced; y: rows, grid-strided) keeps U * (nsrc + 1) independent 16-byte
+// loads in flight per thread and does no 64-bit index division.
+constexpr int RED_THREADS = 256;
+constexpr int RED_U = 4;
 template <int VEC>
-__global__ void reduce_kernel(SrcList srcs, int nsrc, float* dst, int64_t dst_pitch, int64_t rows, int64_t cols) {
+__global__ void __launch_bounds__(RED_THREADS) reduce_kernel(SrcList srcs, int nsrc, float* dst, int64_t dst_pitch,
+                                                             int64_t rows, int64_t cols) {
   const int64_t groups = cols / VEC;
-  const int64_t total = rows * groups;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / groups;
-    const int64_t c = (i - r * groups) * VEC;
+  const int64_t g0 = (int64_t)blockIdx.x * (RED_THREADS * RED_U) + threadIdx.x;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     if constexpr (VEC == 4) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 acc[RED_U];
+#pragma unroll
+      for (int u = 0; u < RED_U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < nsrc; ++s) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(srcs.ptr[s] + r * srcs.pitch[s] + c));
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        const float4* row = reinterpret_cast<const float4*>(srcs.ptr[s] + r * srcs.pitch[s]);
+#pragma unroll
+        for (int u = 0; u < RED_U; ++u) {
+          const int64_t g = g0 + u * RED_THREADS;
+          if (g < groups) {
+            const float4 v = __ldcs(row + g);
+            acc[u].x += v.x; acc[u].y += v.y; acc[u].z += v.z; acc[u].w += v.w;
+          }
+        }
       }
-      float4* d = reinterpret_cast<float4*>(dst + r * dst_pitch + c);
-      float4 o = *d;
-      o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
-      *d = o;
+      float4* drow = reinterpret_cast<float4*>(dst + r * dst_pitch);
+#pragma unroll
+      for (int u = 0; u < RED_U; ++u) {
+        const int64_t g = g0 + u * RED_THREADS;
+        if (g < groups) {
+          float4 o = drow[g];
+          o.x += acc[u].x; o.y += acc[u].y; o.z += acc[u].z; o.w += acc[u].w;
+          drow[g] = o;
+        }
+      }
     } else {
-      float acc = 0.f;
-      for (int s = 0; s < nsrc; ++s) acc += srcs.ptr[s][r * srcs.pitch[s] + c];
-      dst[r * dst_pitch + c] += acc;
+#pragma unroll
+      for (int u = 0; u < RED_U; ++u) {
+        const int64_t c = g0 + u * RED_THREADS;
+        if (c < cols) {
+          float acc = 0.f;
+          for (int s = 0; s < nsrc; ++s) acc += srcs.ptr[s][r * srcs.pitch[s] + c];
+          dst[r * dst_pitch + c] += acc;
+        }
+      }
     }
   }
+}
+
+static dim3 reduce_grid(int64_t rows, int64_t groups, int sms) {
+  const int64_t gx = (groups + RED_THREADS * RED_U - 1) / (RED_THREADS * RED_U);
+  const int64_t want = (int64_t)sms * 8;   // 8 resident blocks of 256 threads per SM
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(rows, std::min<int64_t>(65535, (want + gx - 1) / gx)));
+  return dim3((unsigned)gx, (unsigned)gy, 1);
 }
 
 // Counter-based value generator at GLOBAL coordinates (splitmix64 finaliser),
@@ -192,6 +220,39 @@ extern "C" int um_get(const um_view* src, const um_view* dst, void* stream) {
 }
 
 extern "C" int um_copy(const um_view* src, const um_view* dst, void* stream) { return um_get(src, dst, stream); }
+// cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWriteValue32Fn stream_write_fn() {
+  static StreamWriteValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWriteValue32Fn>(p);
+  });
+  return fn;
+}
+
+extern "C" int um_signal_supported(int32_t device, int32_t* out) {
+  if (!out) return fail(UM_EVALUE, "null out pointer");
+  (void)device;  // 32-bit stream memory operations are core functionality since CUDA 12
+  *out = stream_write_fn() ? 1 : 0;
+  return UM_OK;
+}
+
+extern "C" int um_signal(uint32_t* flag, uint32_t value, void* stream) {
+  if (!flag) return fail(UM_EVALUE, "null flag");
+  if ((reinterpret_cast<uintptr_t>(flag) & 3) != 0) return fail(UM_EVALUE, "flag must be 4-byte aligned");
+  StreamWriteValue32Fn fn = stream_write_fn();
+  if (!fn) return fail(UM_ECUDA, "cuStreamWriteValue32 unavailable");
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                  CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(UM_ECUDA, "cuStreamWriteValue32 failed (code " + std::to_string((int)r) + ")");
+  return UM_OK;
+}
+
 
 extern "C" int um_accumulate(const um_view* src, const um_view* dst, void* stream) {
   int rc;
@@ -204,9 +265,12 @@ extern "C" int um_accumulate(const um_view* src, const um_view* dst, void* strea
   const float* s = static_cast<const float*>(src->base) + src->row_lo * src->pitch + src->col_lo;
   float* d = static_cast<float*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;
   const int vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0 &&
-                  src->pitch % 4 == 0 && dst->pitch % 4 == 0;
+                  src->pitch % 4 == 0 && dst->pitch % 4 == 0 && cols % 4 == 0;
   const int dev = current_device();
-  accumulate_kernel<<<grid_for(rows * (vec ? cols / 4 : cols), dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const int64_t groups = vec ? cols / 4 : cols;
+  const int64_t gx = (groups + 255) / 256;
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(rows, std::min<int64_t>(65535, ((int64_t)num_sms(dev) * 8 + gx - 1) / gx)));
+  accumulate_kernel<<<dim3((unsigned)gx, (unsigned)gy, 1), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       s, src->pitch, d, dst->pitch, rows, cols, vec);
   UM_CUDA_CHECK(cudaGetLastError());
   return UM_OK;
@@ -237,11 +301,11 @@ extern "C" int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32
       vec = vec && (reinterpret_cast<uintptr_t>(sl.ptr[i]) & 15) == 0 && s.pitch % 4 == 0;
     }
     if (vec)
-      reduce_kernel<4><<<grid_for(rows * cols / 4, dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-          sl, n, d, dst->pitch, rows, cols);
+      reduce_kernel<4><<<reduce_grid(rows, cols / 4, num_sms(dev)), RED_THREADS, 0,
+                         reinterpret_cast<cudaStream_t>(stream)>>>(sl, n, d, dst->pitch, rows, cols);
     else
-      reduce_kernel<1><<<grid_for(rows * cols, dev), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-          sl, n, d, dst->pitch, rows, cols);
+      reduce_kernel<1><<<reduce_grid(rows, cols, num_sms(dev)), RED_THREADS, 0,
+                         reinterpret_cast<cudaStream_t>(stream)>>>(sl, n, d, dst->pitch, rows, cols);
     UM_CUDA_CHECK(cudaGetLastError());
   }
   return UM_OK;

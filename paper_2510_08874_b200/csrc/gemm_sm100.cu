@@ -52,8 +52,13 @@ constexpr int BM = 128;       // rows per CTA (UMMA M = BM * CG)
 constexpr int UMMA_N = 256;   // columns per tcgen05.mma (one accumulator)
 constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
-constexpr int EPI_WARPS = 4;
-constexpr int NUM_THREADS = 64 + EPI_WARPS * 32;
+// epilogue warps: 4 (each drains a 32-lane quarter of TMEM, 2 smem boxes) or
+// 8 (two warps per quarter, each owning half the columns; the warp loads its
+// 128 columns of an accumulator into registers in one go and hands TMEM back
+// before the reduce-adds, so the MMA issuer stops waiting on L2 reduce bandwidth)
+// + GET_WARPS warps of the in-kernel get engine (fused K2, see below)
+constexpr int GET_WARPS = 4;
+constexpr int num_threads(int ew) { return 64 + ew * 32 + GET_WARPS * 32; }
 // default rasterisation group: 4 n-tiles (negative = group along n), i.e. a
 // 4-panel slice of B stays hot while A streams; measured best of {-4,4,8,16,32}
 // on cfg2 / 16384^3 / cfg3 shapes with the dynamic scheduler. UM_GEMM_GROUP overrides.
@@ -61,8 +66,11 @@ constexpr int GROUP_M = -4;
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
 
-template <int CG, int NT>
+template <int CG, int NT, int EW = 4>
 struct Cfg {
+  static constexpr int EPI_WARPS = EW;
+  static constexpr int NUM_THREADS = num_threads(EW);
+  static constexpr int EPI_BOXES = EW == 4 ? 2 : 1;           // smem boxes per epilogue warp
   static constexpr int NACC = NT / UMMA_N;                   // accumulators per tile
   static constexpr int NBUF = 2 / NACC;                      // TMEM tile buffers
   static constexpr int STAGES = (CG == 2 && NT == 256) ? 6 : 4;
@@ -71,7 +79,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
   static constexpr int B_BYTES = B_SUBS * SUB_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BOX_BYTES;
+  static constexpr int EPI_BYTES = EW * EPI_BOXES * EPI_BOX_BYTES;
   static constexpr int BAR_BYTES = 256;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static constexpr uint32_t TMEM_COLS = 512;
@@ -91,6 +99,22 @@ struct alignas(16) Work {
   int32_t sched_static, no_end_stagger;  // profiling A/B knobs: static round-robin tiles; no end stagger
   int64_t c_pitch;
   float* c_ptr;
+  const uint32_t* wait_flag;  // non-null: operands are staged by a get; wait for *wait_flag >= wait_value
+  uint32_t wait_value;
+  int32_t a_get, b_get;       // 1-based index of the in-kernel get delivering the operand (0: none)
+  int32_t pad_;
+};
+
+// One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
+// peer or IPC-mapped memory) into a local staging buffer, cut into chunks of
+// rows_per_chunk rows that the get warps of all CTAs take from a counter.
+struct alignas(16) GetDesc {
+  const uint8_t* src;
+  uint8_t* dst;
+  int64_t src_pitch, dst_pitch;   // bytes
+  int32_t rows, row_bytes;
+  int32_t rows_per_chunk, nchunks;
+  int32_t chunk_start, vec;       // vec: 16-byte aligned rows (vector path)
 };
 
 __device__ __forceinline__ int find_work(const Work* works, int nwork, int t) {
@@ -133,21 +157,28 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
 // apart by whole tiles and the panels get re-read from DRAM).
 constexpr int TQ = 4;  // tile-queue depth (producer runs <= 3 tiles ahead of the epilogue)
 
-constexpr int MAX_INLINE_OPS = 8;
+// up to 40 ops travel in the kernel parameters (CUDA >= 12.1 allows 32764
+// bytes of parameters), so a whole rank's op list is normally ONE launch
+constexpr int MAX_INLINE_OPS = UM_GEMM_MAX_INLINE_OPS;
+constexpr int MAX_GETS = UM_GEMM_MAX_GETS;
+constexpr int GET_CHUNK_BYTES = 32 * 1024;
 struct alignas(64) LaunchArgs {
   const Work* works;          // null: use inl_works
   const CUtensorMap* maps;    // null: use inl_maps
   int nwork, total_tiles;
-  int* counters;              // per-stream {tile, done}; left zeroed by the kernel
+  int* counters;              // per-stream {tile, done clusters, get chunk, get done[MAX_GETS]}
+  int ngets, total_chunks;
   CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
   Work inl_works[MAX_INLINE_OPS];
+  GetDesc gets[MAX_GETS];
 };
-static_assert(sizeof(LaunchArgs) <= 4096, "kernel parameter block");
+static_assert(sizeof(LaunchArgs) <= 32764, "kernel parameter block");
 
-template <int CG, int NT>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int CG, int NT, int EW>
+__global__ void __launch_bounds__(num_threads(EW), 1)
     gemm_bf16_kernel(const __grid_constant__ LaunchArgs args) {
-  using C = Cfg<CG, NT>;
+  using C = Cfg<CG, NT, EW>;
+  constexpr int EPI_WARPS = EW;
   // small op lists travel inside the kernel parameters (no per-launch device
   // allocation or host->device copy); larger ones in a global-memory block
   const Work* __restrict__ works = args.works ? args.works : args.inl_works;
@@ -212,6 +243,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
       int stage = 0;
       uint32_t phase = 0;
+      int ready_work = -1;   // highest work index whose get-arrival flag has been observed
       for (int i = 0;; ++i) {
         int t;
         if (leader) {
@@ -246,6 +278,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int w = find_work(works, nwork, t);
         const Work& wk = works[w];
+        if (w > ready_work) {
+          // fused get -> GEMM: this op reads operand slices a get is still
+          // delivering; wait until every chunk of those gets has landed
+          if (wk.wait_flag) ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
+          if (wk.a_get) ptx::wait_count_geq(&args.counters[3 + wk.a_get - 1], args.gets[wk.a_get - 1].nchunks);
+          if (wk.b_get) ptx::wait_count_geq(&args.counters[3 + wk.b_get - 1], args.gets[wk.b_get - 1].nchunks);
+          ready_work = w;
+        }
         const CUtensorMap* ma = &maps[3 * w + 0];
         const CUtensorMap* mbm = &maps[3 * w + 1];
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
@@ -379,12 +419,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
       }
     }
-  } else {
-    // ===================== Epilogue (4 warps) =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+  } else if (warp < 2 + EW) {
+    // ===================== Epilogue (EW warps) =====================
+    const int e = warp - 2;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access (hardware: warp % 4)
+    constexpr int CHUNKS = UMMA_N / 32;                       // 32-column chunks per accumulator
+    constexpr int WCH = EW == 4 ? CHUNKS : CHUNKS / 2;        // chunks per warp per accumulator
+    const int ch0 = EW == 4 ? 0 : (e / 4) * WCH;              // EW == 8: column half of this warp
     const uint64_t cpols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
     uint64_t cpol = cpols[0];
-    uint8_t* ebuf = smem_epi + (warp - 2) * 2 * EPI_BOX_BYTES;
+    uint8_t* ebuf = smem_epi + e * C::EPI_BOXES * EPI_BOX_BYTES;
     const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
     int it = 0;
     int sbuf = 0;
@@ -402,91 +446,183 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int buf = it % C::NBUF;
       const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
       const int row_in_op = mb * BM * CG + (int)cta_rank * BM + q * 32;   // first row of this warp
+
+      // one 32x32 fp32 chunk (lane = row) from registers into C
+      auto emit = [&](const uint32_t (&r)[32], int col0) {
+        if (wk.c_remote == 3) return;  // (profiling only) accumulator dropped: isolates the main loop's cost
+        if (lane == 0) ptx::bulk_wait_read<C::EPI_BOXES - 1>();   // box no longer read by an earlier TMA op
+        __syncwarp();
+        const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES;
+        if (wk.c_remote != 1) {
+          // registers -> swizzled smem box -> TMA reduce-add into C
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            ptx::st_shared_v4(base + lane * 128 + ((i ^ (lane & 7)) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                              r[4 * i + 3]);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            uint8_t* box = ebuf + sbuf * EPI_BOX_BYTES;
+            if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
+              ptx::tma_store_2d(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+            else if (wk.c_pol >= 0)
+              ptx::tma_reduce_add_2d_hint(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op, cpol);
+            else
+              ptx::tma_reduce_add_2d(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+            ptx::bulk_commit();
+          }
+        } else {
+          // fused remote accumulate (K3): red.global.add into the (peer) C tile.
+          // The 32x32 chunk is transposed through swizzled smem so that each
+          // warp-wide red.v4 covers 4 full 128-byte row segments (coalesced
+          // over NVLink / into L2); no async buffer to wait for.
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            ptx::st_shared_v4(base + lane * 128 + ((i ^ (lane & 7)) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
+                              r[4 * i + 3]);
+          __syncwarp();
+          const int c4 = lane & 7;          // 16-byte column group of this lane
+          const int col = col0 + 4 * c4;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3);   // row within the warp's 32
+            const int row = row_in_op + rr;
+            float4 v = ptx::ld_shared_v4f(base + rr * 128 + ((c4 ^ (rr & 7)) << 4));
+            if (row < wk.m && col < wk.n) {
+              float* dst = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0 + col;
+              if (wk.c_vec_ok && col + 4 <= wk.n) {
+                ptx::red_add_v4_f32(dst, v.x, v.y, v.z, v.w);
+              } else {
+                ptx::red_add_f32(dst, v.x);
+                if (col + 1 < wk.n) ptx::red_add_f32(dst + 1, v.y);
+                if (col + 2 < wk.n) ptx::red_add_f32(dst + 2, v.z);
+                if (col + 3 < wk.n) ptx::red_add_f32(dst + 3, v.w);
+              }
+            }
+          }
+          __syncwarp();
+        }
+        sbuf = (sbuf + 1) % C::EPI_BOXES;
+      };
+      // accumulator drained into registers: hand it back to the MMA warp
+      auto release = [&](int j) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          uint64_t* bar = &tmem_empty[C::NACC == 1 ? buf : j];
+          if constexpr (CG == 1) ptx::mbar_arrive(bar);
+          else ptx::mbar_arrive_cluster(bar, 0);
+        }
+      };
+
 #pragma unroll 1
       for (int j = 0; j < C::NACC; ++j) {
         // NACC == 1: one barrier per TMEM buffer; NACC == 2: one per accumulator
         ptx::mbar_wait(&tmem_full[C::NACC == 1 ? buf : j], tph);
         ptx::tc_fence_after();
         const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * UMMA_N;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
         const int col_acc = nb * NT + j * UMMA_N;
-#pragma unroll 1
-        for (int ch = 0; ch < UMMA_N / 32; ++ch) {
-          uint32_t r[32];
-          ptx::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc_col + ch * 32, r);
+        if constexpr (EW == 8) {
+          // whole 128-column share in registers, TMEM released before any reduce
+          uint32_t r[WCH][32];
+#pragma unroll
+          for (int c = 0; c < WCH; ++c) ptx::tmem_ld_32x32b_x32(taddr + (ch0 + c) * 32, r[c]);
           ptx::tmem_ld_wait();
-          if (ch == UMMA_N / 32 - 1) {
-            // accumulator drained into registers: hand it back to the MMA warp
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              uint64_t* bar = &tmem_empty[C::NACC == 1 ? buf : j];
-              if constexpr (CG == 1) ptx::mbar_arrive(bar);
-              else ptx::mbar_arrive_cluster(bar, 0);
-            }
-          }
-          const int col0 = col_acc + ch * 32;
-          if (wk.c_remote == 3) {
-            // (profiling only) accumulator dropped: isolates the main loop's cost
-          } else if (wk.c_remote != 1) {
-            // registers -> swizzled smem box -> TMA reduce-add into C
-            if (lane == 0) ptx::bulk_wait_read<1>();
-            __syncwarp();
-            const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES + lane * 128;
+          release(j);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint32_t addr = base + ((i ^ (lane & 7)) << 4);
-              ptx::st_shared_v4(addr, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
-                ptx::tma_store_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
-              else if (wk.c_pol >= 0)
-                ptx::tma_reduce_add_2d_hint(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op,
-                                            cpol);
-              else
-                ptx::tma_reduce_add_2d(mc, ebuf + sbuf * EPI_BOX_BYTES, wk.c_col0 + col0, wk.c_row0 + row_in_op);
-              ptx::bulk_commit();
-            }
-            sbuf ^= 1;
-          } else {
-            // fused remote accumulate (K3): red.global.add into the (peer) C tile.
-            // The 32x32 chunk is transposed through swizzled smem so that each
-            // warp-wide red.v4 covers 4 full 128-byte row segments (coalesced
-            // over NVLink / into L2); no async buffer to wait for.
-            const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES;
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              ptx::st_shared_v4(base + lane * 128 + ((i ^ (lane & 7)) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2],
-                                r[4 * i + 3]);
-            __syncwarp();
-            const int c4 = lane & 7;          // 16-byte column group of this lane
-            const int col = col0 + 4 * c4;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int rr = i * 4 + (lane >> 3);   // row within the warp's 32
-              const int row = row_in_op + rr;
-              float4 v = ptx::ld_shared_v4f(base + rr * 128 + ((c4 ^ (rr & 7)) << 4));
-              if (row < wk.m && col < wk.n) {
-                float* dst = wk.c_ptr + (int64_t)(wk.c_row0 + row) * wk.c_pitch + wk.c_col0 + col;
-                if (wk.c_vec_ok && col + 4 <= wk.n) {
-                  ptx::red_add_v4_f32(dst, v.x, v.y, v.z, v.w);
-                } else {
-                  ptx::red_add_f32(dst, v.x);
-                  if (col + 1 < wk.n) ptx::red_add_f32(dst + 1, v.y);
-                  if (col + 2 < wk.n) ptx::red_add_f32(dst + 2, v.z);
-                  if (col + 3 < wk.n) ptx::red_add_f32(dst + 3, v.w);
-                }
-              }
-            }
-            sbuf ^= 1;
+          for (int c = 0; c < WCH; ++c) emit(r[c], col_acc + (ch0 + c) * 32);
+        } else {
+#pragma unroll 1
+          for (int ch = 0; ch < CHUNKS; ++ch) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(taddr + ch * 32, r);
+            ptx::tmem_ld_wait();
+            if (ch == CHUNKS - 1) release(j);
+            emit(r, col_acc + ch * 32);
           }
         }
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();
+  } else if (args.ngets > 0) {
+    // ===================== get engine (GET_WARPS warps per CTA) =====================
+    // Pulls the launch's remote operand slices into local staging buffers while
+    // the tensor cores work on ops whose operands are already here.  Chunks are
+    // handed out in get order from a global counter, so every resident CTA
+    // helps and the first ops' operands land first.  No wait on anything but its
+    // own loads: deadlock-free whatever the SMs are doing.
+    int* const chunk_ctr = &args.counters[2];
+    int* const done = &args.counters[3];
+    for (;;) {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(chunk_ctr, 1);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= args.total_chunks) break;
+      int j = 0;
+      while (j + 1 < args.ngets && args.gets[j + 1].chunk_start <= c) ++j;
+      const GetDesc& g = args.gets[j];
+      const int r0 = (c - g.chunk_start) * g.rows_per_chunk;
+      const int r1 = min(g.rows, r0 + g.rows_per_chunk);
+      constexpr int U = 16;  // 16-byte loads in flight per lane (4 warps: 32 KiB per SM)
+      if (g.vec && (g.row_bytes >> 4) >= 32) {
+        // rows of >= 512 B: walk (row, 16-byte column) incrementally, no division
+        const int n16 = g.row_bytes >> 4;
+        int rr = r0, cc = lane;
+        while (rr < r1) {
+          uint4 v[U];
+          int vr[U], vc[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            vr[u] = rr;
+            vc[u] = cc;
+            if (rr < r1) v[u] = ptx::ld_nc_v4(g.src + (int64_t)rr * g.src_pitch + cc * 16);
+            cc += 32;
+            if (cc >= n16) { cc -= n16; ++rr; }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (vr[u] < r1) *reinterpret_cast<uint4*>(g.dst + (int64_t)vr[u] * g.dst_pitch + vc[u] * 16) = v[u];
+        }
+      } else if (g.vec) {
+        const int n16 = g.row_bytes >> 4;
+        const int total = (r1 - r0) * n16;
+        for (int base = lane; base < total; base += 32 * U) {
+          uint4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * 32;
+            if (i < total) {
+              const int rr = i / n16, cc = i - rr * n16;
+              v[u] = ptx::ld_nc_v4(g.src + (int64_t)(r0 + rr) * g.src_pitch + cc * 16);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * 32;
+            if (i < total) {
+              const int rr = i / n16, cc = i - rr * n16;
+              *reinterpret_cast<uint4*>(g.dst + (int64_t)(r0 + rr) * g.dst_pitch + cc * 16) = v[u];
+            }
+          }
+        }
+      } else {
+        // unaligned rows (misaligned partitionings): 2-byte granules
+        const int n2 = g.row_bytes >> 1;
+        const int total = (r1 - r0) * n2;
+        for (int i = lane; i < total; i += 32) {
+          const int rr = i / n2, cc = i - rr * n2;
+          *reinterpret_cast<uint16_t*>(g.dst + (int64_t)(r0 + rr) * g.dst_pitch + cc * 2) =
+              *reinterpret_cast<const uint16_t*>(g.src + (int64_t)(r0 + rr) * g.src_pitch + cc * 2);
+        }
+      }
+      ptx::fence_proxy_async_global();   // these generic writes precede later TMA (async-proxy) reads
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(&done[j], 1);
+      }
+    }
   }
 
   ptx::tc_fence_before();
@@ -560,6 +696,7 @@ static int env_int(const char* name, int dflt) {
 // = 0 normal | 1 evict_first | 2 evict_last (-1 = auto).
 struct Knobs {
   int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 0, sched_static = 0;
+  int epi_warps = 4;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -574,6 +711,7 @@ static const Knobs& knobs() {
     k.cpol = env_int("UM_GEMM_CPOL", -1);
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
+    k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
   });
   return k;
 }
@@ -588,31 +726,33 @@ static int* stream_counters(int device, cudaStream_t stream) {
   for (auto& e : table)
     if (e.first.first == device && e.first.second == stream) return e.second;
   int* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  constexpr size_t bytes = (3 + MAX_GETS) * sizeof(int);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
   // zero in stream order: torch's streams are non-blocking, so a plain
   // cudaMemset (legacy default stream) would race the first launch
-  if (cudaMemsetAsync(p, 0, 2 * sizeof(int), stream) != cudaSuccess) return nullptr;
+  if (cudaMemsetAsync(p, 0, bytes, stream) != cudaSuccess) return nullptr;
   table.push_back({{device, stream}, p});
   return p;
 }
 
-template <int CG, int NT>
+template <int CG, int NT, int EW>
 static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
-  using C = Cfg<CG, NT>;
+  using C = Cfg<CG, NT, EW>;
   const int total_tiles = args.total_tiles;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
   if (!attr_set[device]) {
-    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES));
     attr_set[device] = true;
   }
   int sms = 0;
   UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const int clusters = std::min(total_tiles, sms / CG);
+  // with in-kernel gets every SM joins (its get warps pull even when it gets no tile)
+  const int clusters = args.ngets > 0 ? sms / CG : std::min(total_tiles, sms / CG);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG, 1, 1);
-  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -622,7 +762,7 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT>, args));
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW>, args));
   return UM_OK;
 }
 
@@ -662,7 +802,10 @@ static void pick_variant(const std::vector<um_gemm_op>& ops, int sms, int& cg, i
   nt = tiles512 >= 2 * (sms / 2) ? 512 : 256;
 }
 
-int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t stream) {
+int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in, int ngets, int device,
+                 cudaStream_t stream) {
+  if (ngets < 0 || ngets > MAX_GETS || (ngets > 0 && !gets_in))
+    return fail(UM_EVALUE, "in-kernel get list must hold 0.." + std::to_string(MAX_GETS) + " entries");
   DeviceGuard guard(device);
   // ---- stage misaligned operand slices
   std::vector<um_gemm_op> ops(ops_in, ops_in + nops);
@@ -672,6 +815,10 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
       if (!inner_aligned(*v) && view_rows(*v) > 0 && view_cols(*v) > 0)
         scratch_bytes += (size_t)(view_rows(*v) * aligned_pitch(view_cols(*v), v->dtype) * esize(v->dtype) + 256);
     if (!inner_aligned(op.c)) op.c_remote = 1;
+    if (op.a_get < 0 || op.a_get > ngets || op.b_get < 0 || op.b_get > ngets)
+      return fail(UM_EVALUE, "op references an in-kernel get outside the launch's list");
+    if ((op.a_get && !inner_aligned(op.a)) || (op.b_get && !inner_aligned(op.b)))
+      return fail(UM_ECONTRACT, "an operand delivered by an in-kernel get must be TMA-aligned (16-byte column start)");
   }
   void* scratch = nullptr;
   if (scratch_bytes) {
@@ -761,6 +908,10 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     w.c_col0 = (int32_t)op.c.col_lo;
     w.c_pitch = op.c.pitch;
     w.c_ptr = reinterpret_cast<float*>(op.c.base);
+    w.wait_flag = op.wait_flag;
+    w.wait_value = op.wait_value;
+    w.a_get = op.a_get;
+    w.b_get = op.b_get;
     w.group = kn.group;
     // L2 eviction hints default to normal: measured on the box, evict_last on
     // the group-reused operand + evict_first on the streamed one lowered the
@@ -787,7 +938,7 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     maps.push_back(mbm);
     maps.push_back(mc);
   }
-  if (works.empty()) return UM_OK;
+  if (works.empty() && ngets == 0) return UM_OK;
   static LaunchArgs args;  // host-side staging of the parameter block (calls for a device are serialised)
   static std::mutex args_mu;
   std::lock_guard<std::mutex> lock(args_mu);
@@ -796,6 +947,38 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
   args.total_tiles = total;
   args.counters = stream_counters(device, stream);
   if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
+  // ---- in-kernel gets (fused K2)
+  int chunks = 0;
+  for (int i = 0; i < ngets; ++i) {
+    const um_get_desc& gd = gets_in[i];
+    int rc;
+    if ((rc = check_view(&gd.src, "get src", false)) || (rc = check_view(&gd.dst, "get dst", false))) return rc;
+    if (gd.src.dtype != gd.dst.dtype || view_rows(gd.src) != view_rows(gd.dst) || view_cols(gd.src) != view_cols(gd.dst))
+      return fail(UM_ECONTRACT, "get: src and dst slices differ in dtype or shape");
+    const int64_t es = esize(gd.src.dtype);
+    GetDesc& g = args.gets[i];
+    g.src = static_cast<const uint8_t*>(gd.src.base) + (gd.src.row_lo * gd.src.pitch + gd.src.col_lo) * es;
+    g.dst = static_cast<uint8_t*>(gd.dst.base) + (gd.dst.row_lo * gd.dst.pitch + gd.dst.col_lo) * es;
+    g.src_pitch = gd.src.pitch * es;
+    g.dst_pitch = gd.dst.pitch * es;
+    if (view_rows(gd.src) > INT32_MAX || view_cols(gd.src) * es > INT32_MAX)
+      return fail(UM_EVALUE, "get slice too large");
+    g.rows = (int32_t)view_rows(gd.src);
+    g.row_bytes = (int32_t)(view_cols(gd.src) * es);
+    g.rows_per_chunk = std::max(1, GET_CHUNK_BYTES / std::max(1, g.row_bytes));
+    g.nchunks = g.rows && g.row_bytes ? (g.rows + g.rows_per_chunk - 1) / g.rows_per_chunk : 0;
+    g.chunk_start = chunks;
+    g.vec = ((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) | (uintptr_t)g.src_pitch |
+              (uintptr_t)g.dst_pitch | (uintptr_t)g.row_bytes) & 15) == 0;
+    chunks += g.nchunks;
+  }
+  args.ngets = ngets;
+  args.total_chunks = chunks;
+  if (ngets) UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + ngets) * sizeof(int), stream));
+  if (works.empty()) {
+    // gets only: still one launch (the get warps do the work, no tiles)
+    args.total_tiles = 0;
+  }
   void* dbuf = nullptr;
   if (works.size() <= (size_t)MAX_INLINE_OPS) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
@@ -813,9 +996,11 @@ int launch_batch(const um_gemm_op* ops_in, int nops, int device, cudaStream_t st
     args.works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
   }
   int rc;
-  if (CG == 1) rc = launch<1, 256>(args, device, stream);
-  else if (NT == 512) rc = launch<2, 512>(args, device, stream);
-  else rc = launch<2, 256>(args, device, stream);
+  if (args.total_tiles == 0 && ngets == 0) return UM_OK;
+  if (CG == 1) rc = launch<1, 256, 4>(args, device, stream);
+  else if (NT == 512) rc = kn.epi_warps == 8 ? launch<2, 512, 8>(args, device, stream)
+                                             : launch<2, 512, 4>(args, device, stream);
+  else rc = kn.epi_warps == 8 ? launch<2, 256, 8>(args, device, stream) : launch<2, 256, 4>(args, device, stream);
   if (dbuf) cudaFreeAsync(dbuf, stream);
   return rc;
 }
@@ -830,12 +1015,18 @@ extern "C" int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c,
   op.b = *b;
   op.c = *c;
   op.c_remote = 0;
-  return um::gemm::launch_batch(&op, 1, c->device, reinterpret_cast<cudaStream_t>(stream));
+  return um::gemm::launch_batch(&op, 1, nullptr, 0, c->device, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream) {
   if (nops < 0 || (nops > 0 && !ops)) return um::fail(UM_EVALUE, "bad op list");
-  return um::gemm::launch_batch(ops, nops, device, reinterpret_cast<cudaStream_t>(stream));
+  return um::gemm::launch_batch(ops, nops, nullptr, 0, device, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int um_gemm_acc_fused(const um_gemm_op* ops, int32_t nops, const um_get_desc* gets, int32_t ngets,
+                                 int32_t device, void* stream) {
+  if (nops < 0 || (nops > 0 && !ops)) return um::fail(UM_EVALUE, "bad op list");
+  return um::gemm::launch_batch(ops, nops, gets, ngets, device, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group) {

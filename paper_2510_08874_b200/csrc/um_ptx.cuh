@@ -82,6 +82,57 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
       : "memory");
   return ok != 0;
 }
+// Arrival flag of a one-sided get (K2): spin until *flag has reached `value`
+// (wrap-safe), with acquire semantics, then order the data the flag guards
+// before later async-proxy (TMA) reads.  The flag is written in stream order
+// after the copy-engine transfer (um_signal), so it needs no SM to progress.
+__device__ __forceinline__ void wait_flag_geq(const uint32_t* flag, uint32_t value) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  if ((int32_t)(v - value) < 0) {
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    do {
+      __nanosleep(256);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 20000000000ull) {
+        printf("unimul_b200: get-arrival watchdog fired (block %d, flag %u < %u)\n", blockIdx.x, v, value);
+        __trap();
+      }
+    } while ((int32_t)(v - value) < 0);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Completion count of an in-kernel get: spin until *ctr >= n (acquire), then
+// order the guarded data before later async-proxy (TMA) reads.
+__device__ __forceinline__ void wait_count_geq(const int* ctr, int n) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  if (v < n) {
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    do {
+      __nanosleep(128);
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 20000000000ull) {
+        printf("unimul_b200: in-kernel get watchdog fired (block %d, %d of %d chunks)\n", blockIdx.x, v, n);
+        __trap();
+      }
+    } while (v < n);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait_cluster(addr, parity)) return;

@@ -65,6 +65,13 @@ class ExecConfig:
       fused_accumulate   remote C updates from the K1 epilogue (K3 fused);
                          False = scratch GEMM + um_accumulate.
       reduce_distributed K4 over all replica owners (True) or pull-to-origin.
+      get_engine         "kernel": remote slices are pulled by get warps INSIDE
+                         the K1 launch (um_gemm_acc_fused) and each op starts
+                         when its pulls have landed — one launch per rank (up
+                         to UM_GEMM_MAX_INLINE_OPS ops / UM_GEMM_MAX_GETS pulls)
+                         with the gets overlapping the GEMMs of earlier ops;
+                         "copy": copy-engine pulls on a get stream, the host
+                         splits K1 launches at every pull not yet waited on.
     """
 
     stationarity: Stationarity = Stationarity.STATIONARY_C
@@ -78,6 +85,7 @@ class ExecConfig:
     gemm_batch: int = 0
     fused_accumulate: bool = True
     reduce_distributed: bool = True
+    get_engine: str = "kernel"
 
     def __post_init__(self):
         if self.prefetch_depth < 1 or self.max_inflight_gemms < 1 or self.max_inflight_accums < 1:
@@ -88,6 +96,8 @@ class ExecConfig:
             raise ValueError(f"unknown staging mode {self.staging!r}")
         if self.same_device_gets not in ("copy", "direct"):
             raise ValueError(f"unknown same_device_gets {self.same_device_gets!r}")
+        if self.get_engine not in ("kernel", "copy"):
+            raise ValueError(f"unknown get_engine {self.get_engine!r}")
         if self.gemm_batch < 0:
             raise ValueError("gemm_batch must be >= 0")
 
@@ -307,6 +317,12 @@ def _check_operands(A, B, C):
     A.fabric._require_data()
 
 
+def _tma_ok(v) -> bool:
+    """K1 reads a view in place iff its column start, pitch and base are 16-byte aligned."""
+    es = 2 if v.dtype == _capi.UM_BF16 else 4
+    return (v.col_lo * es) % 16 == 0 and (v.pitch * es) % 16 == 0 and (v.base or 0) % 16 == 0
+
+
 class _RankRun:
     """Device work of one rank's direct schedule (issued asynchronously)."""
 
@@ -331,49 +347,76 @@ class _RankRun:
     def issue(self):
         lib = _capi.load()
         s, st, fab = self.sched, self.stats, self.fab
-        # ---- K2: one pull per remote (matrix, tile), first-use order
-        fetch_events = []
+        nf = len(s.fetches)
+        # staged slice buffers: one per remote (matrix, tile), first-use order
         staged = []
         with torch.cuda.device(self.dev):
             for f in s.fetches:
                 M = self._mat(f.mat)
-                seg = M.segment(f.tile, f.replica)
-                rows, cols = f.r1 - f.r0, f.c1 - f.c0
-                pitch = pitch_for(cols, M.dtype)
-                with torch.cuda.stream(self.gs):
-                    buf = torch.empty((rows, pitch), dtype=M.dtype, device=f"cuda:{self.dev}")
-                buf.record_stream(self.cs)
+                with torch.cuda.stream(self.cs):
+                    buf = torch.empty((f.r1 - f.r0, pitch_for(f.c1 - f.c0, M.dtype)), dtype=M.dtype,
+                                      device=f"cuda:{self.dev}")
+                buf.record_stream(self.gs)
                 self.buffers.append(buf)
-                src = seg.um_view(f.r0, f.r1, f.c0, f.c1)
-                dst = _capi.UmView(buf.data_ptr(), 0, rows, 0, cols, pitch, um_dtype(M.dtype), self.dev)
+                staged.append(buf)
+            views = [(self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged),
+                      self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)) for i, op in enumerate(s.ops)]
+            # which pulls run inside the K1 launch: every op reading the staged
+            # slice must see a TMA-readable view of it (16-byte column start);
+            # the rest go through the copy engines with host-side ordering
+            in_kernel = [self.cfg.get_engine == "kernel"] * nf
+            for i in range(len(s.ops)):
+                for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
+                    if src >= 0 and not _tma_ok(v):
+                        in_kernel[src] = False
+            # ---- K2 on the copy engines (get stream), first-use order
+            fetch_events = [None] * nf
+            for j, f in enumerate(s.fetches):
+                if in_kernel[j]:
+                    continue
+                dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0, staged[j].stride(0),
+                                   um_dtype(staged[j].dtype), self.dev)
+                src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
                 _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(self.gs.cuda_stream)),
                             "um_get")
                 ev = torch.cuda.Event()
                 ev.record(self.gs)
-                fetch_events.append(ev)
-                staged.append(buf)
-                nbytes = rows * cols * buf.element_size()
+                fetch_events[j] = ev
+            for j, f in enumerate(s.fetches):
+                nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
                 fab.counters.add_traffic(self.caller, f.owner, 0, 0, nbytes)
                 st.gets += 1
                 st.staged_bytes += nbytes
-            st.pool_acquired = st.pool_released = st.pool_peak = len(s.fetches)
+            st.pool_acquired = st.pool_released = st.pool_peak = nf
 
-            # ---- K1: grouped launches, flushed when the next op needs an unwaited pull
+            # ---- K1: grouped launches.  In-kernel pulls travel with the first
+            # launch that needs them; a copy-engine pull not yet waited on
+            # splits the launch (the host orders it on the compute stream).
             batch: list = []
+            batch_gets: list = []            # (fetch index) of this launch's in-kernel pulls
+            gets_slot: dict = {}             # fetch index -> 1-based slot in batch_gets
+            launched = [False] * nf          # in-kernel pull issued by an earlier launch
             batch_remote = 0
-            waited = -1
-            cap = self.cfg.gemm_batch or (1 << 30)
+            waited = [False] * nf
+            cap = self.cfg.gemm_batch or _capi.GEMM_MAX_INLINE_OPS
 
             def flush():
-                nonlocal batch, batch_remote
-                if not batch:
+                nonlocal batch, batch_remote, batch_gets, gets_slot
+                if not batch and not batch_gets:
                     return
-                arr = (_capi.UmGemmOp * len(batch))(*batch)
+                arr = (_capi.UmGemmOp * max(1, len(batch)))(*batch)
+                garr = (_capi.UmGetDesc * max(1, len(batch_gets)))()
+                for gi, j in enumerate(batch_gets):
+                    f = s.fetches[j]
+                    garr[gi].src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
+                    garr[gi].dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0,
+                                                staged[j].stride(0), um_dtype(staged[j].dtype), self.dev)
+                    launched[j] = True
                 if TRACE_ENABLED:
                     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     t0.record(self.cs)
-                _capi.check(lib.um_gemm_acc_batch(arr, len(batch), self.dev, ctypes.c_void_p(self.cs.cuda_stream)),
-                            "um_gemm_acc_batch")
+                _capi.check(lib.um_gemm_acc_fused(arr, len(batch), garr, len(batch_gets), self.dev,
+                                                  ctypes.c_void_p(self.cs.cuda_stream)), "um_gemm_acc_fused")
                 if TRACE_ENABLED:
                     t1.record(self.cs)
                     TRACE.append((t0, t1, float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo)
@@ -381,35 +424,53 @@ class _RankRun:
                 st.launches += 1
                 st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
                 st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)
-                batch, batch_remote = [], 0
+                batch, batch_remote, batch_gets, gets_slot = [], 0, [], {}
+
+            def host_wait(j):
+                if not waited[j]:
+                    flush()
+                    self.cs.wait_event(fetch_events[j])
+                    waited[j] = True
 
             for i, op in enumerate(s.ops):
-                need = max(s.a_src[i], s.b_src[i])
-                if need > waited:
-                    flush()
-                    for j in range(waited + 1, need + 1):
-                        self.cs.wait_event(fetch_events[j])
-                    waited = need
+                srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
+                for j in srcs:
+                    if not in_kernel[j]:
+                        host_wait(j)
                 remote = s.c_remote[i] and self.fab.device_of(
                     self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
-                if len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums):
+                new_gets = {j for j in srcs if in_kernel[j] and not launched[j] and j not in gets_slot}
+                if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
+                        or len(batch_gets) + len(new_gets) > _capi.GEMM_MAX_GETS):
                     flush()
-                ga = self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged)
-                gb = self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)
+                    new_gets = {j for j in srcs if in_kernel[j] and not launched[j]}
+                ga, gb = views[i]
                 if remote and not self.cfg.fused_accumulate:
+                    # unfused remote update: its pulls must have landed host-side
+                    flush()
+                    for j in srcs:
+                        if in_kernel[j] and not launched[j]:
+                            batch_gets.append(j)
                     flush()
                     self._scratch_gemm(op, ga, gb)
                     continue
+                for j in sorted(new_gets):
+                    batch_gets.append(j)
+                    gets_slot[j] = len(batch_gets)
                 cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
                 gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
-                batch.append(_capi.UmGemmOp(ga, gb, gc, 1 if remote else 0, 0))
+                g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
+                g.a_get = gets_slot.get(s.a_src[i], 0)
+                g.b_get = gets_slot.get(s.b_src[i], 0)
+                batch.append(g)
                 batch_remote += int(remote)
                 st.executed_ops.append(op)
                 st.a_requests.append(op.a_tile)
                 st.b_requests.append(op.b_tile)
             flush()
-            for j in range(waited + 1, len(fetch_events)):
-                self.cs.wait_event(fetch_events[j])
+            for j in range(nf):
+                if fetch_events[j] is not None and not waited[j]:
+                    self.cs.wait_event(fetch_events[j])
             st.peak_inflight_gemms = 1 if s.ops else 0
             self.done = torch.cuda.Event()
             self.done.record(self.cs)

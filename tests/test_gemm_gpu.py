@@ -109,3 +109,35 @@ def test_one_cta_variant_matches(cuda):
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=300)
     assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
+
+
+def test_wait_flag_orders_op_after_signal(cuda):
+    """um_signal + um_gemm_op.wait_flag: the K1 producer holds the op until a
+    stream-ordered flag write on ANOTHER stream (issued after a device-side
+    delay) reaches the op's wait_value."""
+    import ctypes
+
+    from paper_2510_08874_b200 import _capi
+
+    lib = _capi.load()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = ints(256, 128, g, torch.bfloat16)
+    b = ints(128, 256, g, torch.bfloat16)
+    c = torch.zeros(256, 256, device="cuda")
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s_sig, s_gemm = torch.cuda.Stream(), torch.cuda.Stream()
+    op = _capi.UmGemmOp(_capi.UmView(a.data_ptr(), 0, 256, 0, 128, a.stride(0), _capi.UM_BF16, 0),
+                        _capi.UmView(b.data_ptr(), 0, 128, 0, 256, b.stride(0), _capi.UM_BF16, 0),
+                        _capi.UmView(c.data_ptr(), 0, 256, 0, 256, c.stride(0), _capi.UM_F32, 0), 0)
+    op.wait_flag = flag.data_ptr() + 4
+    op.wait_value = 7
+    with torch.cuda.stream(s_sig):
+        torch.cuda._sleep(20_000_000)         # ~10 ms of device time before the signal
+    _capi.check(lib.um_signal(ctypes.c_void_p(flag.data_ptr() + 4), 7, ctypes.c_void_p(s_sig.cuda_stream)),
+                "um_signal")
+    _capi.check(lib.um_gemm_acc_batch(ctypes.byref(op), 1, 0, ctypes.c_void_p(s_gemm.cuda_stream)),
+                "um_gemm_acc_batch")
+    torch.cuda.synchronize()
+    assert torch.equal(c, ref_acc(torch.zeros_like(c), a, b))
+    assert flag.tolist() == [0, 7, 0, 0]
