@@ -109,6 +109,20 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def k1_traffic(config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the K1 launch from the committed
+    `ncu --set full` capture (profiles/r1_ncu_summary.json), or None if not captured
+    for this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_summary.json")) as f:
+            prof = json.load(f)
+        e = prof.get(f"k1_bench_{config}")
+        return None if e is None else {"bytes_per_launch": e["dram_bytes_per_launch"],
+                                       "source": "profiles/r1_ncu_summary.json:k1_bench_" + config}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def blas_threads(n: int):
     """Use all n host threads in BLAS even under torchrun (which sets OMP_NUM_THREADS=1)."""
     from threadpoolctl import threadpool_limits
@@ -268,6 +282,9 @@ def b200_arm(args):
         rate, sample, cores, _ = cpu_oracle_rate(m, n, k, p, desc, target_s=args.cpu_s)
         cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample}
 
+    traffic = k1_traffic(args.config) if world == 1 else None
+    # A read once, B read once, C read + written once (fp32 C += A.B), per K1 launch
+    algo_bytes = (2 * m * k + 2 * k * n + 8 * m * n) / p
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -279,7 +296,10 @@ def b200_arm(args):
                               m * k * 2 / p / 2**20, m * n * 4 / p / 2**20)},
                "frac_of_peak": value / (world * peak), "peak_per_gpu_tflops": peak, "peak_kind": peak_kind,
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                            "frac": (achieved / peak) if achieved else None, "traffic": None,
+                            "frac": (achieved / peak) if achieved else None,
+                            "traffic": (traffic or {}).get("bytes_per_launch"),
+                            "traffic_source": (traffic or {}).get("source"),
+                            "algorithmic_bytes_per_launch": algo_bytes,
                             "kernel": "um::gemm::gemm_bf16_kernel<2>", "launches_timed": len(durs),
                             "algorithmic_flops_per_launch": (sum(kflops) / len(kflops)) if kflops else None},
                "clocks": clocks, "gpu_launches": launches,

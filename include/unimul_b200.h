@@ -170,6 +170,16 @@ UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device
 UM_API int um_gemm_acc_fused(const um_gemm_op* ops, int32_t nops, const um_get_desc* gets, int32_t ngets,
                              int32_t device, void* stream);
 
+/* Prepared launches: resolve an op/get list once (tensor maps encoded, work
+ * list in the parameter block, persistent device buffers) and replay it with
+ * one call per step.  The views' memory must stay allocated and in place
+ * until um_gemm_destroy (which waits for the device if it owns buffers).
+ * Replay semantics equal um_gemm_acc_fused on the same lists.              */
+UM_API int um_gemm_prepare(const um_gemm_op* ops, int32_t nops, const um_get_desc* gets, int32_t ngets,
+                           int32_t device, void** handle);
+UM_API int um_gemm_launch(void* handle, void* stream);
+UM_API int um_gemm_destroy(void* handle);
+
 /* Tile/stage knobs of the GEMM (bench/profiling): returns 0 and fills.    */
 UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group);
 

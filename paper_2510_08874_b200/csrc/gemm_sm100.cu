@@ -802,11 +802,48 @@ static void pick_variant(const std::vector<um_gemm_op>& ops, int sms, int& cg, i
   nt = tiles512 >= 2 * (sms / 2) ? 512 : 256;
 }
 
-int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in, int ngets, int device,
-                 cudaStream_t stream) {
+// A launch with everything host-side resolved: tensor maps encoded, work
+// list and get descriptors in the parameter block, misaligned operands'
+// staging copies listed.  One-shot calls build, launch and drop it; the
+// runtime keeps one per (rank, schedule) and replays it (um_gemm_prepare /
+// um_gemm_launch), so a repeated multiply costs one launch call on the host.
+struct StageCopy {
+  void* dst;
+  size_t dpitch;
+  const void* src;
+  size_t spitch, width, height;
+};
+struct Prepared {
+  int device = 0, CG = 2, NT = 256, EW = 4, ngets = 0;
+  bool persistent = false, empty = true;
+  void* scratch = nullptr;    // aligned copies of misaligned operand slices
+  void* dbuf = nullptr;       // work list + tensor maps of > MAX_INLINE_OPS ops
+  std::vector<StageCopy> copies;
+  LaunchArgs args;
+};
+
+static void release(Prepared* P, cudaStream_t stream) {
+  if (!P) return;
+  if (P->persistent) {
+    if (P->scratch) cudaFree(P->scratch);
+    if (P->dbuf) cudaFree(P->dbuf);
+  } else {
+    if (P->scratch) cudaFreeAsync(P->scratch, stream);
+    if (P->dbuf) cudaFreeAsync(P->dbuf, stream);
+  }
+  delete P;
+}
+
+// persistent: device-side buffers are cudaMalloc'd and filled synchronously
+// (kept until um_gemm_destroy); else they are stream-ordered on `stream`.
+static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in, int ngets, int device,
+                   bool persistent, cudaStream_t stream, Prepared* P) {
   if (ngets < 0 || ngets > MAX_GETS || (ngets > 0 && !gets_in))
     return fail(UM_EVALUE, "in-kernel get list must hold 0.." + std::to_string(MAX_GETS) + " entries");
   DeviceGuard guard(device);
+  P->device = device;
+  P->persistent = persistent;
+  memset(&P->args, 0, sizeof(P->args));
   // ---- stage misaligned operand slices
   std::vector<um_gemm_op> ops(ops_in, ops_in + nops);
   size_t scratch_bytes = 0;
@@ -822,7 +859,9 @@ int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in,
   }
   void* scratch = nullptr;
   if (scratch_bytes) {
-    UM_CUDA_CHECK(cudaMallocAsync(&scratch, scratch_bytes, stream));
+    if (persistent) UM_CUDA_CHECK(cudaMalloc(&scratch, scratch_bytes));
+    else UM_CUDA_CHECK(cudaMallocAsync(&scratch, scratch_bytes, stream));
+    P->scratch = scratch;
     size_t off = 0;
     for (auto& op : ops)
       for (um_view* v : {&op.a, &op.b}) {
@@ -839,26 +878,22 @@ int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in,
         dst.dtype = v->dtype;
         dst.device = device;
         const int64_t es = esize(v->dtype);
-        UM_CUDA_CHECK(cudaMemcpy2DAsync(dst.base, dst.pitch * es,
-                                        static_cast<const char*>(v->base) + (v->row_lo * v->pitch + v->col_lo) * es,
-                                        v->pitch * es, view_cols(*v) * es, view_rows(*v), cudaMemcpyDefault, stream));
+        P->copies.push_back({dst.base, (size_t)(dst.pitch * es),
+                             static_cast<const char*>(v->base) + (v->row_lo * v->pitch + v->col_lo) * es,
+                             (size_t)(v->pitch * es), (size_t)(view_cols(*v) * es), (size_t)view_rows(*v)});
         off += (size_t)(dst.row_hi * dst.pitch * es + 255) / 256 * 256;
         *v = dst;
       }
   }
-  struct ScratchFree {
-    void* p;
-    cudaStream_t s;
-    ~ScratchFree() {
-      if (p) cudaFreeAsync(p, s);
-    }
-  } scratch_guard{scratch, stream};
 
   int sms = 0;
   UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   int CG = 2, NT = 256;
   pick_variant(ops, sms, CG, NT);
   const Knobs& kn = knobs();
+  P->CG = CG;
+  P->NT = NT;
+  P->EW = (CG == 2 && kn.epi_warps == 8) ? 8 : 4;
 
   std::vector<Work> works;
   std::vector<CUtensorMap> maps;
@@ -938,15 +973,9 @@ int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in,
     maps.push_back(mbm);
     maps.push_back(mc);
   }
-  if (works.empty() && ngets == 0) return UM_OK;
-  static LaunchArgs args;  // host-side staging of the parameter block (calls for a device are serialised)
-  static std::mutex args_mu;
-  std::lock_guard<std::mutex> lock(args_mu);
-  memset(&args, 0, sizeof(args));
+  LaunchArgs& args = P->args;
   args.nwork = (int)works.size();
   args.total_tiles = total;
-  args.counters = stream_counters(device, stream);
-  if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
   // ---- in-kernel gets (fused K2)
   int chunks = 0;
   for (int i = 0; i < ngets; ++i) {
@@ -974,11 +1003,8 @@ int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in,
   }
   args.ngets = ngets;
   args.total_chunks = chunks;
-  if (ngets) UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + ngets) * sizeof(int), stream));
-  if (works.empty()) {
-    // gets only: still one launch (the get warps do the work, no tiles)
-    args.total_tiles = 0;
-  }
+  P->ngets = ngets;
+  P->empty = total == 0 && ngets == 0;   // gets only: still one launch (get warps, no tiles)
   void* dbuf = nullptr;
   if (works.size() <= (size_t)MAX_INLINE_OPS) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
@@ -990,18 +1016,42 @@ int launch_batch(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_in,
     std::vector<uint8_t> host(maps_bytes + works_bytes);
     memcpy(host.data(), maps.data(), maps_bytes);
     memcpy(host.data() + maps_bytes, works.data(), works_bytes);
-    UM_CUDA_CHECK(cudaMallocAsync(&dbuf, host.size(), stream));
-    UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
+    if (persistent) {
+      UM_CUDA_CHECK(cudaMalloc(&dbuf, host.size()));
+      P->dbuf = dbuf;
+      UM_CUDA_CHECK(cudaMemcpy(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice));
+    } else {
+      UM_CUDA_CHECK(cudaMallocAsync(&dbuf, host.size(), stream));
+      P->dbuf = dbuf;
+      UM_CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
+    }
     args.maps = reinterpret_cast<const CUtensorMap*>(dbuf);
     args.works = reinterpret_cast<const Work*>(reinterpret_cast<uint8_t*>(dbuf) + maps_bytes);
   }
-  int rc;
-  if (args.total_tiles == 0 && ngets == 0) return UM_OK;
-  if (CG == 1) rc = launch<1, 256, 4>(args, device, stream);
-  else if (NT == 512) rc = kn.epi_warps == 8 ? launch<2, 512, 8>(args, device, stream)
-                                             : launch<2, 512, 4>(args, device, stream);
-  else rc = kn.epi_warps == 8 ? launch<2, 256, 8>(args, device, stream) : launch<2, 256, 4>(args, device, stream);
-  if (dbuf) cudaFreeAsync(dbuf, stream);
+  return UM_OK;
+}
+
+static int launch_prepared(Prepared* P, cudaStream_t stream) {
+  if (P->empty) return UM_OK;
+  DeviceGuard guard(P->device);
+  for (const StageCopy& c : P->copies)
+    UM_CUDA_CHECK(cudaMemcpy2DAsync(c.dst, c.dpitch, c.src, c.spitch, c.width, c.height, cudaMemcpyDefault, stream));
+  LaunchArgs& args = P->args;
+  args.counters = stream_counters(P->device, stream);
+  if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
+  if (P->ngets) UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + P->ngets) * sizeof(int), stream));
+  if (P->CG == 1) return launch<1, 256, 4>(args, P->device, stream);
+  if (P->NT == 512)
+    return P->EW == 8 ? launch<2, 512, 8>(args, P->device, stream) : launch<2, 512, 4>(args, P->device, stream);
+  return P->EW == 8 ? launch<2, 256, 8>(args, P->device, stream) : launch<2, 256, 4>(args, P->device, stream);
+}
+
+int launch_batch(const um_gemm_op* ops, int nops, const um_get_desc* gets, int ngets, int device,
+                 cudaStream_t stream) {
+  Prepared* P = new Prepared();
+  int rc = prepare(ops, nops, gets, ngets, device, false, stream, P);
+  if (rc == UM_OK) rc = launch_prepared(P, stream);
+  release(P, stream);
   return rc;
 }
 
@@ -1027,6 +1077,36 @@ extern "C" int um_gemm_acc_fused(const um_gemm_op* ops, int32_t nops, const um_g
                                  int32_t device, void* stream) {
   if (nops < 0 || (nops > 0 && !ops)) return um::fail(UM_EVALUE, "bad op list");
   return um::gemm::launch_batch(ops, nops, gets, ngets, device, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int um_gemm_prepare(const um_gemm_op* ops, int32_t nops, const um_get_desc* gets, int32_t ngets,
+                               int32_t device, void** handle) {
+  if (!handle) return um::fail(UM_EVALUE, "null handle pointer");
+  if (nops < 0 || (nops > 0 && !ops)) return um::fail(UM_EVALUE, "bad op list");
+  auto* P = new um::gemm::Prepared();
+  int rc = um::gemm::prepare(ops, nops, gets, ngets, device, true, nullptr, P);
+  if (rc != UM_OK) {
+    um::gemm::release(P, nullptr);
+    *handle = nullptr;
+    return rc;
+  }
+  *handle = P;
+  return UM_OK;
+}
+
+extern "C" int um_gemm_launch(void* handle, void* stream) {
+  if (!handle) return um::fail(UM_EVALUE, "null launch handle");
+  return um::gemm::launch_prepared(static_cast<um::gemm::Prepared*>(handle), reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int um_gemm_destroy(void* handle) {
+  if (handle) {
+    auto* P = static_cast<um::gemm::Prepared*>(handle);
+    um::DeviceGuard guard(P->device);
+    if (P->scratch || P->dbuf) cudaDeviceSynchronize();   // buffers may still be read by a launch
+    um::gemm::release(P, nullptr);
+  }
+  return UM_OK;
 }
 
 extern "C" int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group) {

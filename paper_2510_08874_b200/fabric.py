@@ -164,6 +164,14 @@ class FabricCounters:
             self.msgs[initiator, peer] += nmsgs
             self.wire_bytes[initiator, peer] += wire
 
+    def merge(self, other: "FabricCounters"):
+        """Add another counter set (same rank count) into this one."""
+        with self._lock:
+            self.bytes += other.bytes
+            self.msgs += other.msgs
+            self.wire_bytes += other.wire_bytes
+            self.flops += other.flops
+
     def add_flops(self, rank: int, flops: int):
         with self._lock:
             self.flops[rank] += flops

@@ -272,11 +272,25 @@ def _count_reference_traffic(A, B, C, cfg: ExecConfig, sched: DirectSchedule):
     Every remote A/B tile is a whole-tile get per op (runtime.py:427-438,
     distmatrix.py:158); every remote C update one accumulate_tile
     (runtime.py:338-341: one message if full-width, else one per row;
-    2x bytes and messages in LOCK_GET_PUT, fabric.py:225-234).
+    2x bytes and messages in LOCK_GET_PUT, fabric.py:225-234).  The per-rank
+    totals are computed once per schedule and accumulation mode and added in
+    one step per run (the host issue path stays O(1) in the op count).
     """
     ctr = A.fabric.counters
-    caller = sched.caller
     lgp = cfg.accumulate_mode is AccumulateMode.LOCK_GET_PUT
+    memo = sched.__dict__.setdefault("traffic_memo", {})
+    delta = memo.get(lgp)
+    if delta is None:
+        from paper_2510_08874_b200.fabric import FabricCounters
+
+        tmp = FabricCounters(ctr.nprocs)
+        _reference_traffic_into(tmp, A, B, C, lgp, sched)
+        delta = memo[lgp] = tmp
+    ctr.merge(delta)
+
+
+def _reference_traffic_into(ctr, A, B, C, lgp: bool, sched: DirectSchedule):
+    caller = sched.caller
     for i, op in enumerate(sched.ops):
         for M, t in ((A, op.a_tile), (B, op.b_tile)):
             owner = M.owner_rank(t, M.replica_of(caller))
@@ -323,6 +337,31 @@ def _tma_ok(v) -> bool:
     return (v.col_lo * es) % 16 == 0 and (v.pitch * es) % 16 == 0 and (v.base or 0) % 16 == 0
 
 
+class _IssuePlan:
+    """One rank's issue plan: persistent staging buffers, copy-engine pulls,
+    and an action list of prepared K1 launches / stream waits / unfused
+    scratch updates, replayed by every multiply with the same schedule."""
+
+    def __init__(self, nprocs: int):
+        from paper_2510_08874_b200.fabric import FabricCounters
+
+        self.staged: list = []
+        self.host_fetches: list = []      # (fetch index, src view, dst view)
+        self.actions: list = []           # ("launch", handle, flops) | ("wait", j) | ("scratch", op, ga, gb)
+        self.final_waits: list = []
+        self.handles: list = []
+        self.traffic = FabricCounters(nprocs)   # wire bytes of the pulls, added per run
+        self.stats = RunStats()
+
+    def __del__(self):
+        try:
+            lib = _capi.load()
+            for h in self.handles:
+                lib.um_gemm_destroy(ctypes.c_void_p(h))
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
 class _RankRun:
     """Device work of one rank's direct schedule (issued asynchronously)."""
 
@@ -345,11 +384,25 @@ class _RankRun:
         return self.A if name == "A" else self.B
 
     def issue(self):
+        """Replay this rank's issue plan (built once per schedule and knob set)."""
+        key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate)
+        plans = self.sched.__dict__.setdefault("plans", {})
+        plan = plans.get(key)
+        if plan is None:
+            plan = plans[key] = self._build_plan()
+        self._replay(plan)
+        return self
+
+    def _build_plan(self) -> "_IssuePlan":
+        """Resolve everything host-side once: persistent staging buffers (the
+        paper's pre-allocated pool), which pulls run inside
+        the GEMM launch and which on the copy engines, the launch split, and one
+        prepared K1 launch (um_gemm_prepare) per group."""
         lib = _capi.load()
-        s, st, fab = self.sched, self.stats, self.fab
+        s, fab = self.sched, self.fab
         nf = len(s.fetches)
-        # staged slice buffers: one per remote (matrix, tile), first-use order
-        staged = []
+        plan = _IssuePlan(fab.counters.nprocs)
+        st = plan.stats
         with torch.cuda.device(self.dev):
             for f in s.fetches:
                 M = self._mat(f.mat)
@@ -357,124 +410,150 @@ class _RankRun:
                     buf = torch.empty((f.r1 - f.r0, pitch_for(f.c1 - f.c0, M.dtype)), dtype=M.dtype,
                                       device=f"cuda:{self.dev}")
                 buf.record_stream(self.gs)
-                self.buffers.append(buf)
-                staged.append(buf)
-            views = [(self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged),
-                      self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)) for i, op in enumerate(s.ops)]
-            # which pulls run inside the K1 launch: every op reading the staged
-            # slice must see a TMA-readable view of it (16-byte column start);
-            # the rest go through the copy engines with host-side ordering
-            in_kernel = [self.cfg.get_engine == "kernel"] * nf
-            for i in range(len(s.ops)):
-                for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
-                    if src >= 0 and not _tma_ok(v):
-                        in_kernel[src] = False
-            # ---- K2 on the copy engines (get stream), first-use order
-            fetch_events = [None] * nf
-            for j, f in enumerate(s.fetches):
-                if in_kernel[j]:
-                    continue
-                dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0, staged[j].stride(0),
-                                   um_dtype(staged[j].dtype), self.dev)
-                src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
-                _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(self.gs.cuda_stream)),
-                            "um_get")
+                plan.staged.append(buf)
+        staged = plan.staged
+        views = [(self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged),
+                  self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)) for i, op in enumerate(s.ops)]
+        # which pulls run inside the K1 launch: every op reading the staged slice
+        # must see a TMA-readable view of it (16-byte column start); the rest go
+        # through the copy engines with host-side ordering
+        in_kernel = [self.cfg.get_engine == "kernel"] * nf
+        for i in range(len(s.ops)):
+            for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
+                if src >= 0 and not _tma_ok(v):
+                    in_kernel[src] = False
+
+        def fetch_views(j):
+            f = s.fetches[j]
+            src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
+            dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0, staged[j].stride(0),
+                               um_dtype(staged[j].dtype), self.dev)
+            return src, dst
+
+        for j, f in enumerate(s.fetches):
+            if not in_kernel[j]:
+                plan.host_fetches.append((j, *fetch_views(j)))
+            nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
+            plan.traffic.add_traffic(self.caller, f.owner, 0, 0, nbytes)
+            st.gets += 1
+            st.staged_bytes += nbytes
+        st.pool_acquired = st.pool_released = st.pool_peak = nf
+
+        # ---- K1 launch groups.  In-kernel pulls travel with the first launch
+        # that needs them; a copy-engine pull not yet waited on splits the group
+        # (the compute stream waits for its event).
+        batch: list = []
+        batch_gets: list = []            # fetch indices of this launch's in-kernel pulls
+        gets_slot: dict = {}             # fetch index -> 1-based slot in batch_gets
+        launched = [False] * nf
+        batch_remote = 0
+        waited = [False] * nf
+        cap = self.cfg.gemm_batch or _capi.GEMM_MAX_INLINE_OPS
+
+        def flush():
+            nonlocal batch, batch_remote, batch_gets, gets_slot
+            if not batch and not batch_gets:
+                return
+            arr = (_capi.UmGemmOp * max(1, len(batch)))(*batch)
+            garr = (_capi.UmGetDesc * max(1, len(batch_gets)))()
+            for gi, j in enumerate(batch_gets):
+                garr[gi].src, garr[gi].dst = fetch_views(j)
+                launched[j] = True
+            h = ctypes.c_void_p()
+            _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, len(batch_gets), self.dev, ctypes.byref(h)),
+                        "um_gemm_prepare")
+            plan.handles.append(h.value)
+            flops = float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo) * (g.b.col_hi - g.b.col_lo)
+                              for g in batch))
+            plan.actions.append(("launch", h.value, flops))
+            st.launches += 1
+            st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
+            st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)
+            batch, batch_remote, batch_gets, gets_slot = [], 0, [], {}
+
+        def host_wait(j):
+            if not waited[j]:
+                flush()
+                plan.actions.append(("wait", j))
+                waited[j] = True
+
+        for i, op in enumerate(s.ops):
+            srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
+            for j in srcs:
+                if not in_kernel[j]:
+                    host_wait(j)
+            remote = s.c_remote[i] and self.fab.device_of(
+                self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
+            new_gets = {j for j in srcs if in_kernel[j] and not launched[j] and j not in gets_slot}
+            if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
+                    or len(batch_gets) + len(new_gets) > _capi.GEMM_MAX_GETS):
+                flush()
+                new_gets = {j for j in srcs if in_kernel[j] and not launched[j]}
+            ga, gb = views[i]
+            st.executed_ops.append(op)
+            st.a_requests.append(op.a_tile)
+            st.b_requests.append(op.b_tile)
+            if remote and not self.cfg.fused_accumulate:
+                # unfused remote update (scratch GEMM + K3): its pulls must have landed
+                flush()
+                for j in srcs:
+                    if in_kernel[j] and not launched[j]:
+                        batch_gets.append(j)
+                flush()
+                plan.actions.append(("scratch", op, ga, gb))
+                st.launches += 2
+                st.peak_ops_per_launch = max(st.peak_ops_per_launch, 1)
+                st.peak_inflight_accums = max(st.peak_inflight_accums, 1)
+                continue
+            for j in sorted(new_gets):
+                batch_gets.append(j)
+                gets_slot[j] = len(batch_gets)
+            cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+            gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+            g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
+            g.a_get = gets_slot.get(s.a_src[i], 0)
+            g.b_get = gets_slot.get(s.b_src[i], 0)
+            batch.append(g)
+            batch_remote += int(remote)
+        flush()
+        plan.final_waits = [j for j in range(nf) if not in_kernel[j] and not waited[j]]
+        st.peak_inflight_gemms = 1 if s.ops else 0
+        return plan
+
+    def _replay(self, plan: "_IssuePlan"):
+        lib = _capi.load()
+        fab = self.fab
+        with torch.cuda.device(self.dev):
+            events = {}
+            gsp = ctypes.c_void_p(self.gs.cuda_stream)
+            for j, src, dst in plan.host_fetches:        # K2 on the copy engines, first-use order
+                _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get")
                 ev = torch.cuda.Event()
                 ev.record(self.gs)
-                fetch_events[j] = ev
-            for j, f in enumerate(s.fetches):
-                nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
-                fab.counters.add_traffic(self.caller, f.owner, 0, 0, nbytes)
-                st.gets += 1
-                st.staged_bytes += nbytes
-            st.pool_acquired = st.pool_released = st.pool_peak = nf
-
-            # ---- K1: grouped launches.  In-kernel pulls travel with the first
-            # launch that needs them; a copy-engine pull not yet waited on
-            # splits the launch (the host orders it on the compute stream).
-            batch: list = []
-            batch_gets: list = []            # (fetch index) of this launch's in-kernel pulls
-            gets_slot: dict = {}             # fetch index -> 1-based slot in batch_gets
-            launched = [False] * nf          # in-kernel pull issued by an earlier launch
-            batch_remote = 0
-            waited = [False] * nf
-            cap = self.cfg.gemm_batch or _capi.GEMM_MAX_INLINE_OPS
-
-            def flush():
-                nonlocal batch, batch_remote, batch_gets, gets_slot
-                if not batch and not batch_gets:
-                    return
-                arr = (_capi.UmGemmOp * max(1, len(batch)))(*batch)
-                garr = (_capi.UmGetDesc * max(1, len(batch_gets)))()
-                for gi, j in enumerate(batch_gets):
-                    f = s.fetches[j]
-                    garr[gi].src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
-                    garr[gi].dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0,
-                                                staged[j].stride(0), um_dtype(staged[j].dtype), self.dev)
-                    launched[j] = True
-                if TRACE_ENABLED:
-                    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    t0.record(self.cs)
-                _capi.check(lib.um_gemm_acc_fused(arr, len(batch), garr, len(batch_gets), self.dev,
-                                                  ctypes.c_void_p(self.cs.cuda_stream)), "um_gemm_acc_fused")
-                if TRACE_ENABLED:
-                    t1.record(self.cs)
-                    TRACE.append((t0, t1, float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo)
-                                                    * (g.b.col_hi - g.b.col_lo) for g in batch))))
-                st.launches += 1
-                st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
-                st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)
-                batch, batch_remote, batch_gets, gets_slot = [], 0, [], {}
-
-            def host_wait(j):
-                if not waited[j]:
-                    flush()
-                    self.cs.wait_event(fetch_events[j])
-                    waited[j] = True
-
-            for i, op in enumerate(s.ops):
-                srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
-                for j in srcs:
-                    if not in_kernel[j]:
-                        host_wait(j)
-                remote = s.c_remote[i] and self.fab.device_of(
-                    self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
-                new_gets = {j for j in srcs if in_kernel[j] and not launched[j] and j not in gets_slot}
-                if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
-                        or len(batch_gets) + len(new_gets) > _capi.GEMM_MAX_GETS):
-                    flush()
-                    new_gets = {j for j in srcs if in_kernel[j] and not launched[j]}
-                ga, gb = views[i]
-                if remote and not self.cfg.fused_accumulate:
-                    # unfused remote update: its pulls must have landed host-side
-                    flush()
-                    for j in srcs:
-                        if in_kernel[j] and not launched[j]:
-                            batch_gets.append(j)
-                    flush()
-                    self._scratch_gemm(op, ga, gb)
-                    continue
-                for j in sorted(new_gets):
-                    batch_gets.append(j)
-                    gets_slot[j] = len(batch_gets)
-                cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
-                gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
-                g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
-                g.a_get = gets_slot.get(s.a_src[i], 0)
-                g.b_get = gets_slot.get(s.b_src[i], 0)
-                batch.append(g)
-                batch_remote += int(remote)
-                st.executed_ops.append(op)
-                st.a_requests.append(op.a_tile)
-                st.b_requests.append(op.b_tile)
-            flush()
-            for j in range(nf):
-                if fetch_events[j] is not None and not waited[j]:
-                    self.cs.wait_event(fetch_events[j])
-            st.peak_inflight_gemms = 1 if s.ops else 0
+                events[j] = ev
+            csp = ctypes.c_void_p(self.cs.cuda_stream)
+            for act in plan.actions:
+                if act[0] == "launch":
+                    if TRACE_ENABLED:
+                        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        t0.record(self.cs)
+                    _capi.check(lib.um_gemm_launch(ctypes.c_void_p(act[1]), csp), "um_gemm_launch")
+                    if TRACE_ENABLED:
+                        t1.record(self.cs)
+                        TRACE.append((t0, t1, act[2]))
+                elif act[0] == "wait":
+                    self.cs.wait_event(events[act[1]])
+                else:
+                    self._scratch_gemm(*act[1:])
+            for j in plan.final_waits:
+                self.cs.wait_event(events[j])
             self.done = torch.cuda.Event()
             self.done.record(self.cs)
-        return self
+        fab.counters.merge(plan.traffic)
+        t = plan.stats
+        self.stats = RunStats(list(t.executed_ops), list(t.a_requests), list(t.b_requests), t.peak_inflight_gemms,
+                              t.peak_inflight_accums, t.pool_acquired, t.pool_released, t.pool_peak, 0, t.gets,
+                              t.staged_bytes, t.launches, t.peak_ops_per_launch)
 
     def _operand_view(self, name, t, loc, src_idx, staged):
         M = self._mat(name)
@@ -502,13 +581,6 @@ class _RankRun:
         with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
             _capi.check(lib.um_accumulate(ctypes.byref(gs), ctypes.byref(dst), ctypes.c_void_p(self.cs.cuda_stream)),
                         "um_accumulate")
-        st = self.stats
-        st.launches += 2
-        st.peak_ops_per_launch = max(st.peak_ops_per_launch, 1)
-        st.peak_inflight_accums = max(st.peak_inflight_accums, 1)
-        st.executed_ops.append(op)
-        st.a_requests.append(op.a_tile)
-        st.b_requests.append(op.b_tile)
 
 
 def run_direct(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
