@@ -133,8 +133,9 @@ typedef struct {
   int32_t c_remote;
   uint32_t wait_value;
   const uint32_t* wait_flag;
-  int32_t a_get, b_get;    /* um_gemm_acc_fused: 1-based index of the get that delivers
-                              this op's a / b operand (0 = already resident)            */
+  int32_t a_get, b_get;    /* um_gemm_acc_fused: 1 if this op's a / b operand is written by an
+                              in-kernel get of the same launch (must then be TMA-aligned) */
+  uint64_t get_mask;       /* bit i: the op starts loading only after gets[i] has landed  */
 } um_gemm_op;
 
 /* A pull executed INSIDE the GEMM launch (um_gemm_acc_fused): src slice
@@ -162,7 +163,7 @@ UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device
 
 /* Fused get -> GEMM: ONE persistent launch that pulls `gets` with dedicated
  * get warps on every SM (chunks handed out in list order) while the tensor
- * cores run the ops; an op whose a_get/b_get names a pull starts loading
+ * cores run the ops; an op whose get_mask names pulls starts loading
  * only after every chunk of that pull has landed (device-side acquire), so
  * the reference's ordering rule "a compute depends on completion of its input
  * fetches" (runtime.py:219-236) holds without host round trips.

@@ -15,7 +15,9 @@ import os
 from paper_2510_08874_b200.errors import ConfigError, ContractError, OwnershipError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libunimul_b200.so")
+# UNIMUL_B200_LIB points at an alternative build of the same library (A/B
+# experiments with compile-time variants); the default is the in-tree build.
+LIB_PATH = os.environ.get("UNIMUL_B200_LIB") or os.path.join(_HERE, "_lib", "libunimul_b200.so")
 
 UM_OK = 0
 UM_ECONFIG = 1
@@ -68,7 +70,8 @@ class UmView(ctypes.Structure):
 class UmGemmOp(ctypes.Structure):
     _fields_ = [("a", UmView), ("b", UmView), ("c", UmView),
                 ("c_remote", ctypes.c_int32), ("wait_value", ctypes.c_uint32),
-                ("wait_flag", ctypes.c_void_p), ("a_get", ctypes.c_int32), ("b_get", ctypes.c_int32)]
+                ("wait_flag", ctypes.c_void_p), ("a_get", ctypes.c_int32), ("b_get", ctypes.c_int32),
+                ("get_mask", ctypes.c_uint64)]
 
 
 class UmGetDesc(ctypes.Structure):

@@ -57,7 +57,10 @@ constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 // 128 columns of an accumulator into registers in one go and hands TMEM back
 // before the reduce-adds, so the MMA issuer stops waiting on L2 reduce bandwidth)
 // + GET_WARPS warps of the in-kernel get engine (fused K2, see below)
-constexpr int GET_WARPS = 4;
+#ifndef UM_GET_WARPS
+#define UM_GET_WARPS 4
+#endif
+constexpr int GET_WARPS = UM_GET_WARPS;
 constexpr int num_threads(int ew) { return 64 + ew * 32 + GET_WARPS * 32; }
 // default rasterisation group: 4 n-tiles (negative = group along n), i.e. a
 // 4-panel slice of B stays hot while A streams; measured best of {-4,4,8,16,32}
@@ -101,8 +104,8 @@ struct alignas(16) Work {
   float* c_ptr;
   const uint32_t* wait_flag;  // non-null: operands are staged by a get; wait for *wait_flag >= wait_value
   uint32_t wait_value;
-  int32_t a_get, b_get;       // 1-based index of the in-kernel get delivering the operand (0: none)
   int32_t pad_;
+  uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -282,8 +285,10 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           // fused get -> GEMM: this op reads operand slices a get is still
           // delivering; wait until every chunk of those gets has landed
           if (wk.wait_flag) ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
-          if (wk.a_get) ptx::wait_count_geq(&args.counters[3 + wk.a_get - 1], args.gets[wk.a_get - 1].nchunks);
-          if (wk.b_get) ptx::wait_count_geq(&args.counters[3 + wk.b_get - 1], args.gets[wk.b_get - 1].nchunks);
+          for (uint64_t msk = wk.wait_mask; msk; msk &= msk - 1) {
+            const int gi = __ffsll((long long)msk) - 1;
+            ptx::wait_count_geq(&args.counters[3 + gi], args.gets[gi].nchunks);
+          }
           ready_work = w;
         }
         const CUtensorMap* ma = &maps[3 * w + 0];
@@ -565,35 +570,25 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
       const int r0 = (c - g.chunk_start) * g.rows_per_chunk;
       const int r1 = min(g.rows, r0 + g.rows_per_chunk);
       constexpr int U = 16;  // 16-byte loads in flight per lane (4 warps: 32 KiB per SM)
-      if (g.vec && (g.row_bytes >> 4) >= 32) {
-        // rows of >= 512 B: walk (row, 16-byte column) incrementally, no division
+      if (g.vec) {
+        // flat (row, 16-byte column) walk of the chunk; the division by the row
+        // width is a float reciprocal + one-step fix-up (exact: i < 2^24)
         const int n16 = g.row_bytes >> 4;
-        int rr = r0, cc = lane;
-        while (rr < r1) {
-          uint4 v[U];
-          int vr[U], vc[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            vr[u] = rr;
-            vc[u] = cc;
-            if (rr < r1) v[u] = ptx::ld_nc_v4(g.src + (int64_t)rr * g.src_pitch + cc * 16);
-            cc += 32;
-            if (cc >= n16) { cc -= n16; ++rr; }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (vr[u] < r1) *reinterpret_cast<uint4*>(g.dst + (int64_t)vr[u] * g.dst_pitch + vc[u] * 16) = v[u];
-        }
-      } else if (g.vec) {
-        const int n16 = g.row_bytes >> 4;
+        const float inv = 1.0f / (float)n16;
         const int total = (r1 - r0) * n16;
+        auto split = [&](int i, int& rr, int& cc) {
+          rr = __float2int_rz((float)i * inv);
+          cc = i - rr * n16;
+          if (cc < 0) { --rr; cc += n16; } else if (cc >= n16) { ++rr; cc -= n16; }
+        };
         for (int base = lane; base < total; base += 32 * U) {
           uint4 v[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int i = base + u * 32;
             if (i < total) {
-              const int rr = i / n16, cc = i - rr * n16;
+              int rr, cc;
+              split(i, rr, cc);
               v[u] = ptx::ld_nc_v4(g.src + (int64_t)(r0 + rr) * g.src_pitch + cc * 16);
             }
           }
@@ -601,7 +596,8 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           for (int u = 0; u < U; ++u) {
             const int i = base + u * 32;
             if (i < total) {
-              const int rr = i / n16, cc = i - rr * n16;
+              int rr, cc;
+              split(i, rr, cc);
               *reinterpret_cast<uint4*>(g.dst + (int64_t)(r0 + rr) * g.dst_pitch + cc * 16) = v[u];
             }
           }
@@ -852,8 +848,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
       if (!inner_aligned(*v) && view_rows(*v) > 0 && view_cols(*v) > 0)
         scratch_bytes += (size_t)(view_rows(*v) * aligned_pitch(view_cols(*v), v->dtype) * esize(v->dtype) + 256);
     if (!inner_aligned(op.c)) op.c_remote = 1;
-    if (op.a_get < 0 || op.a_get > ngets || op.b_get < 0 || op.b_get > ngets)
-      return fail(UM_EVALUE, "op references an in-kernel get outside the launch's list");
+    if (ngets < 64 && (op.get_mask >> ngets) != 0)
+      return fail(UM_EVALUE, "op waits on an in-kernel get outside the launch's list");
     if ((op.a_get && !inner_aligned(op.a)) || (op.b_get && !inner_aligned(op.b)))
       return fail(UM_ECONTRACT, "an operand delivered by an in-kernel get must be TMA-aligned (16-byte column start)");
   }
@@ -945,8 +941,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.c_ptr = reinterpret_cast<float*>(op.c.base);
     w.wait_flag = op.wait_flag;
     w.wait_value = op.wait_value;
-    w.a_get = op.a_get;
-    w.b_get = op.b_get;
+    w.wait_mask = op.get_mask;
     w.group = kn.group;
     // L2 eviction hints default to normal: measured on the box, evict_last on
     // the group-reused operand + evict_first on the streamed one lowered the

@@ -107,20 +107,23 @@ __device__ __forceinline__ void wait_flag_geq(const uint32_t* flag, uint32_t val
 // Completion count of an in-kernel get: spin until *ctr >= n (acquire), then
 // order the guarded data before later async-proxy (TMA) reads.
 __device__ __forceinline__ void wait_count_geq(const int* ctr, int n) {
+  // relaxed polling (an acquire load invalidates the SM's L1 on every poll),
+  // one acquire fence once the count is reached
   int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
   if (v < n) {
     const uint64_t t0 = globaltimer();
     uint32_t spins = 0;
     do {
       __nanosleep(128);
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
       if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 20000000000ull) {
         printf("unimul_b200: in-kernel get watchdog fired (block %d, %d of %d chunks)\n", blockIdx.x, v, n);
         __trap();
       }
     } while (v < n);
   }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 

@@ -423,29 +423,66 @@ class _RankRun:
                 if src >= 0 and not _tma_ok(v):
                     in_kernel[src] = False
 
-        def fetch_views(j):
+        def fetch_views(j, band=None):
             f = s.fetches[j]
-            src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0, f.r1, f.c0, f.c1)
-            dst = _capi.UmView(staged[j].data_ptr(), 0, f.r1 - f.r0, 0, f.c1 - f.c0, staged[j].stride(0),
+            br0, br1, bc0, bc1 = band if band is not None else (0, f.r1 - f.r0, 0, f.c1 - f.c0)
+            src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0 + br0, f.r0 + br1, f.c0 + bc0, f.c0 + bc1)
+            dst = _capi.UmView(staged[j].data_ptr(), br0, br1, bc0, bc1, staged[j].stride(0),
                                um_dtype(staged[j].dtype), self.dev)
             return src, dst
+
+        # in-kernel pulls are cut into bands along the dimension in which the
+        # ops' slices differ, so an op waits only for the slab it reads (cfg5:
+        # a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
+        uses = [[] for _ in range(nf)]
+        for i, op in enumerate(s.ops):
+            for src, loc in ((s.a_src[i], op.a_local), (s.b_src[i], op.b_local)):
+                if src >= 0:
+                    f = s.fetches[src]
+                    uses[src].append((i, loc.rows.lo - f.r0, loc.rows.hi - f.r0, loc.cols.lo - f.c0,
+                                      loc.cols.hi - f.c0))
+        bands = [None] * nf              # per fetch: list of (r0, r1, c0, c1) in staged-buffer coordinates
+        need = {}                        # (op, fetch) -> band indices
+        for j, f in enumerate(s.fetches):
+            if not in_kernel[j]:
+                continue
+            H, W = f.r1 - f.r0, f.c1 - f.c0
+            sl = uses[j]
+            if all(c0 == 0 and c1 == W for _, _, _, c0, c1 in sl):
+                cuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
+                cand = [(lo, hi, 0, W) for lo, hi in zip(cuts, cuts[1:])]
+                key = lambda bd, u: bd[0] < u[2] and u[1] < bd[1]          # noqa: E731
+            elif all(r0 == 0 and r1 == H for _, r0, r1, _, _ in sl):
+                cuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
+                cand = [(0, H, lo, hi) for lo, hi in zip(cuts, cuts[1:])]
+                key = lambda bd, u: bd[2] < u[4] and u[3] < bd[3]          # noqa: E731
+            else:
+                cand, key = [(0, H, 0, W)], (lambda bd, u: True)
+            cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop bands no op reads
+            if len(cand) > 16:
+                cand, key = [(0, H, 0, W)], (lambda bd, u: True)
+            bands[j] = cand
+            for u in sl:
+                need[(u[0], j)] = [k for k, bd in enumerate(cand) if key(bd, u)]
 
         for j, f in enumerate(s.fetches):
             if not in_kernel[j]:
                 plan.host_fetches.append((j, *fetch_views(j)))
-            nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
+                nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
+            else:
+                nbytes = sum((r1 - r0) * (c1 - c0) for r0, r1, c0, c1 in bands[j]) * staged[j].element_size()
             plan.traffic.add_traffic(self.caller, f.owner, 0, 0, nbytes)
             st.gets += 1
             st.staged_bytes += nbytes
         st.pool_acquired = st.pool_released = st.pool_peak = nf
 
-        # ---- K1 launch groups.  In-kernel pulls travel with the first launch
-        # that needs them; a copy-engine pull not yet waited on splits the group
-        # (the compute stream waits for its event).
+        # ---- K1 launch groups.  In-kernel pulls (bands) travel with the first
+        # launch that needs them; a copy-engine pull not yet waited on splits
+        # the group (the compute stream waits for its event).
         batch: list = []
-        batch_gets: list = []            # fetch indices of this launch's in-kernel pulls
-        gets_slot: dict = {}             # fetch index -> 1-based slot in batch_gets
-        launched = [False] * nf
+        batch_gets: list = []            # (fetch, band) units of this launch, in first-use order
+        gets_slot: dict = {}             # unit -> 0-based slot in batch_gets
+        launched: set = set()
         batch_remote = 0
         waited = [False] * nf
         cap = self.cfg.gemm_batch or _capi.GEMM_MAX_INLINE_OPS
@@ -456,9 +493,9 @@ class _RankRun:
                 return
             arr = (_capi.UmGemmOp * max(1, len(batch)))(*batch)
             garr = (_capi.UmGetDesc * max(1, len(batch_gets)))()
-            for gi, j in enumerate(batch_gets):
-                garr[gi].src, garr[gi].dst = fetch_views(j)
-                launched[j] = True
+            for gi, (j, k) in enumerate(batch_gets):
+                garr[gi].src, garr[gi].dst = fetch_views(j, bands[j][k])
+                launched.add((j, k))
             h = ctypes.c_void_p()
             _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, len(batch_gets), self.dev, ctypes.byref(h)),
                         "um_gemm_prepare")
@@ -484,11 +521,12 @@ class _RankRun:
                     host_wait(j)
             remote = s.c_remote[i] and self.fab.device_of(
                 self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
-            new_gets = {j for j in srcs if in_kernel[j] and not launched[j] and j not in gets_slot}
+            units = [(j, k) for j in dict.fromkeys(srcs) if in_kernel[j] for k in need[(i, j)]]
+            new_units = [u for u in units if u not in launched and u not in gets_slot]
             if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
-                    or len(batch_gets) + len(new_gets) > _capi.GEMM_MAX_GETS):
+                    or len(batch_gets) + len(new_units) > _capi.GEMM_MAX_GETS):
                 flush()
-                new_gets = {j for j in srcs if in_kernel[j] and not launched[j]}
+                new_units = [u for u in units if u not in launched]
             ga, gb = views[i]
             st.executed_ops.append(op)
             st.a_requests.append(op.a_tile)
@@ -496,23 +534,22 @@ class _RankRun:
             if remote and not self.cfg.fused_accumulate:
                 # unfused remote update (scratch GEMM + K3): its pulls must have landed
                 flush()
-                for j in srcs:
-                    if in_kernel[j] and not launched[j]:
-                        batch_gets.append(j)
+                batch_gets.extend(new_units)
                 flush()
                 plan.actions.append(("scratch", op, ga, gb))
                 st.launches += 2
                 st.peak_ops_per_launch = max(st.peak_ops_per_launch, 1)
                 st.peak_inflight_accums = max(st.peak_inflight_accums, 1)
                 continue
-            for j in sorted(new_gets):
-                batch_gets.append(j)
-                gets_slot[j] = len(batch_gets)
+            for u in new_units:
+                gets_slot[u] = len(batch_gets)
+                batch_gets.append(u)
             cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
             gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
             g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
-            g.a_get = gets_slot.get(s.a_src[i], 0)
-            g.b_get = gets_slot.get(s.b_src[i], 0)
+            g.a_get = int(s.a_src[i] >= 0 and in_kernel[s.a_src[i]])
+            g.b_get = int(s.b_src[i] >= 0 and in_kernel[s.b_src[i]])
+            g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot)
             batch.append(g)
             batch_remote += int(remote)
         flush()
