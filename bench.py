@@ -357,7 +357,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--panels", type=int, default=8, help="row panels of the host-streaming e2e path")
+    ap.add_argument("--panels", type=int, default=32, help="row panels of the host-streaming e2e path")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="target seconds per reference-arm step")

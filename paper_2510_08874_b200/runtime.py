@@ -65,6 +65,11 @@ class ExecConfig:
       fused_accumulate   remote C updates from the K1 epilogue (K3 fused);
                          False = scratch GEMM + um_accumulate.
       reduce_distributed K4 over all replica owners (True) or pull-to-origin.
+      mn_split           max sub-ops along m (pulled A dominates) or n (pulled
+                         B dominates) for an op whose first use pulls >= 64
+                         MiB: each sub-op starts when its band has landed.
+      k_split            > 1: split such ops along k instead (one A and one B
+                         slab per sub-op, one extra C read-modify-write each).
       get_engine         "kernel": remote slices are pulled by get warps INSIDE
                          the K1 launch (um_gemm_acc_fused) and each op starts
                          when its pulls have landed — one launch per rank (up
@@ -86,6 +91,8 @@ class ExecConfig:
     fused_accumulate: bool = True
     reduce_distributed: bool = True
     get_engine: str = "kernel"
+    mn_split: int = 4
+    k_split: int = 0
 
     def __post_init__(self):
         if self.prefetch_depth < 1 or self.max_inflight_gemms < 1 or self.max_inflight_accums < 1:
@@ -98,6 +105,8 @@ class ExecConfig:
             raise ValueError(f"unknown same_device_gets {self.same_device_gets!r}")
         if self.get_engine not in ("kernel", "copy"):
             raise ValueError(f"unknown get_engine {self.get_engine!r}")
+        if self.k_split < 0 or self.mn_split < 0:
+            raise ValueError("k_split / mn_split must be >= 0")
         if self.gemm_batch < 0:
             raise ValueError("gemm_batch must be >= 0")
 
@@ -331,6 +340,10 @@ def _check_operands(A, B, C):
     A.fabric._require_data()
 
 
+_SPLIT_BYTES = 64 << 20       # an op whose first use pulls at least this much runs as sub-ops
+_SPLIT_MIN = 2048             # minimum extent of a sub-op along the split dimension
+
+
 def _tma_ok(v) -> bool:
     """K1 reads a view in place iff its column start, pitch and base are 16-byte aligned."""
     es = 2 if v.dtype == _capi.UM_BF16 else 4
@@ -385,7 +398,8 @@ class _RankRun:
 
     def issue(self):
         """Replay this rank's issue plan (built once per schedule and knob set)."""
-        key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate)
+        key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
+               self.cfg.k_split, self.cfg.mn_split, _SPLIT_BYTES, _SPLIT_MIN)
         plans = self.sched.__dict__.setdefault("plans", {})
         plan = plans.get(key)
         if plan is None:
@@ -431,18 +445,62 @@ class _RankRun:
                                um_dtype(staged[j].dtype), self.dev)
             return src, dst
 
-        # in-kernel pulls are cut into bands along the dimension in which the
-        # ops' slices differ, so an op waits only for the slab it reads (cfg5:
-        # a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
-        uses = [[] for _ in range(nf)]
+        # Sub-ops: an op that must first pull a large amount (cfg4: whole 8192^2
+        # A and B tiles) runs as sub-ops that each wait only for their part of
+        # the pull.  Default split: along m when the pulled A dominates, along n
+        # when B does (rows / columns of C: no extra C traffic, the tensor cores
+        # start once B / A and the first A / B band have landed).  k_split > 1
+        # instead cuts k into slabs (every sub-op waits for one A and one B
+        # slab, at the price of one more fp32 C read-modify-write per slab).
+        first_user: dict = {}
+        for i in range(len(s.ops)):
+            for j in (s.a_src[i], s.b_src[i]):
+                if j >= 0:
+                    first_user.setdefault(j, i)
+
+        def pulled(i, j):
+            if j < 0 or not in_kernel[j] or first_user[j] != i:
+                return 0
+            f = s.fetches[j]
+            return (f.r1 - f.r0) * (f.c1 - f.c0) * 2
+
+        items = []                       # (op, sub, dm0, dm1, dn0, dn1, k0, k1), offsets relative to the op
         for i, op in enumerate(s.ops):
-            for src, loc in ((s.a_src[i], op.a_local), (s.b_src[i], op.b_local)):
+            mlen, nlen, klen = len(op.m_bound), len(op.n_bound), len(op.k_bound)
+            pa = pulled(i, s.a_src[i])
+            pb = pulled(i, s.b_src[i]) if s.b_src[i] != s.a_src[i] else 0
+            unfused_remote = s.c_remote[i] and not self.cfg.fused_accumulate
+            nsub, dim = 1, None
+            if not unfused_remote and pa + pb >= _SPLIT_BYTES:
+                if self.cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
+                    nsub, dim = int(min(self.cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
+                elif self.cfg.mn_split > 1 and pa >= pb and mlen >= 2 * _SPLIT_MIN:
+                    nsub, dim = int(min(self.cfg.mn_split, mlen // _SPLIT_MIN)), "m"
+                elif self.cfg.mn_split > 1 and pb > pa and nlen >= 2 * _SPLIT_MIN:
+                    nsub, dim = int(min(self.cfg.mn_split, nlen // _SPLIT_MIN)), "n"
+            full = {"m": mlen, "n": nlen, "k": klen}
+            cut = sorted({0, full[dim]} | {full[dim] * t // nsub // 64 * 64 for t in range(1, nsub)}) if dim else [0, 0]
+            for t in range(len(cut) - 1):
+                lo, hi = cut[t], cut[t + 1]
+                mm = (lo, hi) if dim == "m" else (0, mlen)
+                nn = (lo, hi) if dim == "n" else (0, nlen)
+                kk = (lo, hi) if dim == "k" else (0, klen)
+                items.append((i, t, *mm, *nn, *kk))
+
+        # in-kernel pulls are cut into bands along the dimension in which the
+        # (sub-)ops' slices differ, so an op waits only for the slab it reads
+        # (cfg5: a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
+        uses = [[] for _ in range(nf)]
+        for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
+            op = s.ops[i]
+            a, b = op.a_local, op.b_local
+            for src, (r0, r1, c0, c1) in ((s.a_src[i], (a.rows.lo + m0, a.rows.lo + m1, a.cols.lo + k0, a.cols.lo + k1)),
+                                          (s.b_src[i], (b.rows.lo + k0, b.rows.lo + k1, b.cols.lo + n0, b.cols.lo + n1))):
                 if src >= 0:
                     f = s.fetches[src]
-                    uses[src].append((i, loc.rows.lo - f.r0, loc.rows.hi - f.r0, loc.cols.lo - f.c0,
-                                      loc.cols.hi - f.c0))
+                    uses[src].append((it, r0 - f.r0, r1 - f.r0, c0 - f.c0, c1 - f.c0))
         bands = [None] * nf              # per fetch: list of (r0, r1, c0, c1) in staged-buffer coordinates
-        need = {}                        # (op, fetch) -> band indices
+        need = {}                        # (item, fetch) -> band indices
         for j, f in enumerate(s.fetches):
             if not in_kernel[j]:
                 continue
@@ -514,23 +572,31 @@ class _RankRun:
                 plan.actions.append(("wait", j))
                 waited[j] = True
 
-        for i, op in enumerate(s.ops):
+        for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
+            op = s.ops[i]
             srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
             for j in srcs:
                 if not in_kernel[j]:
                     host_wait(j)
             remote = s.c_remote[i] and self.fab.device_of(
                 self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
-            units = [(j, k) for j in dict.fromkeys(srcs) if in_kernel[j] for k in need[(i, j)]]
+            units = [(j, k) for j in dict.fromkeys(srcs) if in_kernel[j] for k in need[(it, j)]]
             new_units = [u for u in units if u not in launched and u not in gets_slot]
             if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
                     or len(batch_gets) + len(new_units) > _capi.GEMM_MAX_GETS):
                 flush()
                 new_units = [u for u in units if u not in launched]
             ga, gb = views[i]
-            st.executed_ops.append(op)
-            st.a_requests.append(op.a_tile)
-            st.b_requests.append(op.b_tile)
+            sub = (m0, m1, n0, n1, k0, k1) != (0, len(op.m_bound), 0, len(op.n_bound), 0, len(op.k_bound))
+            if sub:
+                ga = _capi.UmView(ga.base, ga.row_lo + m0, ga.row_lo + m1, ga.col_lo + k0, ga.col_lo + k1, ga.pitch,
+                                  ga.dtype, ga.device)
+                gb = _capi.UmView(gb.base, gb.row_lo + k0, gb.row_lo + k1, gb.col_lo + n0, gb.col_lo + n1, gb.pitch,
+                                  gb.dtype, gb.device)
+            if t == 0:
+                st.executed_ops.append(op)
+                st.a_requests.append(op.a_tile)
+                st.b_requests.append(op.b_tile)
             if remote and not self.cfg.fused_accumulate:
                 # unfused remote update (scratch GEMM + K3): its pulls must have landed
                 flush()
@@ -545,7 +611,8 @@ class _RankRun:
                 gets_slot[u] = len(batch_gets)
                 batch_gets.append(u)
             cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
-            gc = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+            cl = op.c_local
+            gc = cseg.um_view(cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
             g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
             g.a_get = int(s.a_src[i] >= 0 and in_kernel[s.a_src[i]])
             g.b_get = int(s.b_src[i] >= 0 and in_kernel[s.b_src[i]])

@@ -13,7 +13,7 @@ from paper_2510_08874_b200.cli import build_problem  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 engine = sys.argv[3] if len(sys.argv) > 3 else "kernel"
-extra = dict(kv.split("=", 1) for kv in sys.argv[4:])      # e.g. same_device_gets=direct
+extra = {k: (int(v) if v.isdigit() else v) for k, v in (kv.split("=", 1) for kv in sys.argv[4:])}
 m, n, k, ap, bp, cp, fa, fb, fc, desc = bench.CONFIGS[name]
 fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, fa(p), fb(p), fc(p), seed=0, real=True, synthetic=True,
                                    devices=[0])

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_runtime_gpu.py tests/test_fullsize_gpu.py -x -q -p no:cacheprovider > gpurun_out/t25.log 2>&1; echo "[tests rc=$?]"; tail -3 gpurun_out/t25.log
+for X in "" "mn_split=0" "k_split=2"; do echo "== $X"; timeout 120 python tools/solo_probe.py cfg4 8 kernel $X 2>&1 | grep -v CUDAEvent.h | grep "rank 3\|rank 5\|rank 7"; done
+timeout 120 python tools/solo_probe.py cfg5 8 kernel 2>&1 | grep -v CUDAEvent.h | tail -2
