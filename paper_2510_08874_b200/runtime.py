@@ -350,6 +350,99 @@ def _tma_ok(v) -> bool:
     return (v.col_lo * es) % 16 == 0 and (v.pitch * es) % 16 == 0 and (v.base or 0) % 16 == 0
 
 
+def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig):
+    """Host-only planning of a rank's in-kernel pulls (no device work).
+
+    Returns (items, bands, need):
+      items  (op, sub, m0, m1, n0, n1, k0, k1): the ops in execution order, an
+             op that must first pull >= _SPLIT_BYTES split into sub-ops
+             (offsets relative to the op's m / n / k ranges);
+      bands  per fetch: (r0, r1, c0, c1) rectangles of the staged slice, cut
+             along the dimension in which the (sub-)ops' slices differ, bands
+             no op reads dropped (None for copy-engine fetches);
+      need   (item, fetch) -> indices of the bands the item reads.
+    """
+    nf = len(s.fetches)
+    # Sub-ops: an op that must first pull a large amount (cfg4: whole 8192^2
+    # A and B tiles) runs as sub-ops that each wait only for their part of
+    # the pull.  Default split: along m when the pulled A dominates, along n
+    # when B does (rows / columns of C: no extra C traffic, the tensor cores
+    # start once B / A and the first A / B band have landed).  k_split > 1
+    # instead cuts k into slabs (every sub-op waits for one A and one B
+    # slab, at the price of one more fp32 C read-modify-write per slab).
+    first_user: dict = {}
+    for i in range(len(s.ops)):
+        for j in (s.a_src[i], s.b_src[i]):
+            if j >= 0:
+                first_user.setdefault(j, i)
+
+    def pulled(i, j):
+        if j < 0 or not in_kernel[j] or first_user[j] != i:
+            return 0
+        f = s.fetches[j]
+        return (f.r1 - f.r0) * (f.c1 - f.c0) * 2
+
+    items = []                       # (op, sub, dm0, dm1, dn0, dn1, k0, k1), offsets relative to the op
+    for i, op in enumerate(s.ops):
+        mlen, nlen, klen = len(op.m_bound), len(op.n_bound), len(op.k_bound)
+        pa = pulled(i, s.a_src[i])
+        pb = pulled(i, s.b_src[i]) if s.b_src[i] != s.a_src[i] else 0
+        unfused_remote = s.c_remote[i] and not cfg.fused_accumulate
+        nsub, dim = 1, None
+        if not unfused_remote and pa + pb >= _SPLIT_BYTES:
+            if cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
+            elif cfg.mn_split > 1 and pa >= pb and mlen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.mn_split, mlen // _SPLIT_MIN)), "m"
+            elif cfg.mn_split > 1 and pb > pa and nlen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.mn_split, nlen // _SPLIT_MIN)), "n"
+        full = {"m": mlen, "n": nlen, "k": klen}
+        cut = sorted({0, full[dim]} | {full[dim] * t // nsub // 64 * 64 for t in range(1, nsub)}) if dim else [0, 0]
+        for t in range(len(cut) - 1):
+            lo, hi = cut[t], cut[t + 1]
+            mm = (lo, hi) if dim == "m" else (0, mlen)
+            nn = (lo, hi) if dim == "n" else (0, nlen)
+            kk = (lo, hi) if dim == "k" else (0, klen)
+            items.append((i, t, *mm, *nn, *kk))
+
+    # in-kernel pulls are cut into bands along the dimension in which the
+    # (sub-)ops' slices differ, so an op waits only for the slab it reads
+    # (cfg5: a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
+    uses = [[] for _ in range(nf)]
+    for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
+        op = s.ops[i]
+        a, b = op.a_local, op.b_local
+        for src, (r0, r1, c0, c1) in ((s.a_src[i], (a.rows.lo + m0, a.rows.lo + m1, a.cols.lo + k0, a.cols.lo + k1)),
+                                      (s.b_src[i], (b.rows.lo + k0, b.rows.lo + k1, b.cols.lo + n0, b.cols.lo + n1))):
+            if src >= 0:
+                f = s.fetches[src]
+                uses[src].append((it, r0 - f.r0, r1 - f.r0, c0 - f.c0, c1 - f.c0))
+    bands = [None] * nf              # per fetch: list of (r0, r1, c0, c1) in staged-buffer coordinates
+    need = {}                        # (item, fetch) -> band indices
+    for j, f in enumerate(s.fetches):
+        if not in_kernel[j]:
+            continue
+        H, W = f.r1 - f.r0, f.c1 - f.c0
+        sl = uses[j]
+        if all(c0 == 0 and c1 == W for _, _, _, c0, c1 in sl):
+            cuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
+            cand = [(lo, hi, 0, W) for lo, hi in zip(cuts, cuts[1:])]
+            key = lambda bd, u: bd[0] < u[2] and u[1] < bd[1]          # noqa: E731
+        elif all(r0 == 0 and r1 == H for _, r0, r1, _, _ in sl):
+            cuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
+            cand = [(0, H, lo, hi) for lo, hi in zip(cuts, cuts[1:])]
+            key = lambda bd, u: bd[2] < u[4] and u[3] < bd[3]          # noqa: E731
+        else:
+            cand, key = [(0, H, 0, W)], (lambda bd, u: True)
+        cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop bands no op reads
+        if len(cand) > 16:
+            cand, key = [(0, H, 0, W)], (lambda bd, u: True)
+        bands[j] = cand
+        for u in sl:
+            need[(u[0], j)] = [k for k, bd in enumerate(cand) if key(bd, u)]
+    return items, bands, need
+
+
 class _IssuePlan:
     """One rank's issue plan: persistent staging buffers, copy-engine pulls,
     and an action list of prepared K1 launches / stream waits / unfused
@@ -445,83 +538,7 @@ class _RankRun:
                                um_dtype(staged[j].dtype), self.dev)
             return src, dst
 
-        # Sub-ops: an op that must first pull a large amount (cfg4: whole 8192^2
-        # A and B tiles) runs as sub-ops that each wait only for their part of
-        # the pull.  Default split: along m when the pulled A dominates, along n
-        # when B does (rows / columns of C: no extra C traffic, the tensor cores
-        # start once B / A and the first A / B band have landed).  k_split > 1
-        # instead cuts k into slabs (every sub-op waits for one A and one B
-        # slab, at the price of one more fp32 C read-modify-write per slab).
-        first_user: dict = {}
-        for i in range(len(s.ops)):
-            for j in (s.a_src[i], s.b_src[i]):
-                if j >= 0:
-                    first_user.setdefault(j, i)
-
-        def pulled(i, j):
-            if j < 0 or not in_kernel[j] or first_user[j] != i:
-                return 0
-            f = s.fetches[j]
-            return (f.r1 - f.r0) * (f.c1 - f.c0) * 2
-
-        items = []                       # (op, sub, dm0, dm1, dn0, dn1, k0, k1), offsets relative to the op
-        for i, op in enumerate(s.ops):
-            mlen, nlen, klen = len(op.m_bound), len(op.n_bound), len(op.k_bound)
-            pa = pulled(i, s.a_src[i])
-            pb = pulled(i, s.b_src[i]) if s.b_src[i] != s.a_src[i] else 0
-            unfused_remote = s.c_remote[i] and not self.cfg.fused_accumulate
-            nsub, dim = 1, None
-            if not unfused_remote and pa + pb >= _SPLIT_BYTES:
-                if self.cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
-                    nsub, dim = int(min(self.cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
-                elif self.cfg.mn_split > 1 and pa >= pb and mlen >= 2 * _SPLIT_MIN:
-                    nsub, dim = int(min(self.cfg.mn_split, mlen // _SPLIT_MIN)), "m"
-                elif self.cfg.mn_split > 1 and pb > pa and nlen >= 2 * _SPLIT_MIN:
-                    nsub, dim = int(min(self.cfg.mn_split, nlen // _SPLIT_MIN)), "n"
-            full = {"m": mlen, "n": nlen, "k": klen}
-            cut = sorted({0, full[dim]} | {full[dim] * t // nsub // 64 * 64 for t in range(1, nsub)}) if dim else [0, 0]
-            for t in range(len(cut) - 1):
-                lo, hi = cut[t], cut[t + 1]
-                mm = (lo, hi) if dim == "m" else (0, mlen)
-                nn = (lo, hi) if dim == "n" else (0, nlen)
-                kk = (lo, hi) if dim == "k" else (0, klen)
-                items.append((i, t, *mm, *nn, *kk))
-
-        # in-kernel pulls are cut into bands along the dimension in which the
-        # (sub-)ops' slices differ, so an op waits only for the slab it reads
-        # (cfg5: a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
-        uses = [[] for _ in range(nf)]
-        for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
-            op = s.ops[i]
-            a, b = op.a_local, op.b_local
-            for src, (r0, r1, c0, c1) in ((s.a_src[i], (a.rows.lo + m0, a.rows.lo + m1, a.cols.lo + k0, a.cols.lo + k1)),
-                                          (s.b_src[i], (b.rows.lo + k0, b.rows.lo + k1, b.cols.lo + n0, b.cols.lo + n1))):
-                if src >= 0:
-                    f = s.fetches[src]
-                    uses[src].append((it, r0 - f.r0, r1 - f.r0, c0 - f.c0, c1 - f.c0))
-        bands = [None] * nf              # per fetch: list of (r0, r1, c0, c1) in staged-buffer coordinates
-        need = {}                        # (item, fetch) -> band indices
-        for j, f in enumerate(s.fetches):
-            if not in_kernel[j]:
-                continue
-            H, W = f.r1 - f.r0, f.c1 - f.c0
-            sl = uses[j]
-            if all(c0 == 0 and c1 == W for _, _, _, c0, c1 in sl):
-                cuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
-                cand = [(lo, hi, 0, W) for lo, hi in zip(cuts, cuts[1:])]
-                key = lambda bd, u: bd[0] < u[2] and u[1] < bd[1]          # noqa: E731
-            elif all(r0 == 0 and r1 == H for _, r0, r1, _, _ in sl):
-                cuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
-                cand = [(0, H, lo, hi) for lo, hi in zip(cuts, cuts[1:])]
-                key = lambda bd, u: bd[2] < u[4] and u[3] < bd[3]          # noqa: E731
-            else:
-                cand, key = [(0, H, 0, W)], (lambda bd, u: True)
-            cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop bands no op reads
-            if len(cand) > 16:
-                cand, key = [(0, H, 0, W)], (lambda bd, u: True)
-            bands[j] = cand
-            for u in sl:
-                need[(u[0], j)] = [k for k, bd in enumerate(cand) if key(bd, u)]
+        items, bands, need = plan_bands(s, in_kernel, self.cfg)
 
         for j, f in enumerate(s.fetches):
             if not in_kernel[j]:
