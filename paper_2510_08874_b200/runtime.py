@@ -424,19 +424,18 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig):
             continue
         H, W = f.r1 - f.r0, f.c1 - f.c0
         sl = uses[j]
-        if all(c0 == 0 and c1 == W for _, _, _, c0, c1 in sl):
-            cuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
-            cand = [(lo, hi, 0, W) for lo, hi in zip(cuts, cuts[1:])]
-            key = lambda bd, u: bd[0] < u[2] and u[1] < bd[1]          # noqa: E731
-        elif all(r0 == 0 and r1 == H for _, r0, r1, _, _ in sl):
-            cuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
-            cand = [(0, H, lo, hi) for lo, hi in zip(cuts, cuts[1:])]
-            key = lambda bd, u: bd[2] < u[4] and u[3] < bd[3]          # noqa: E731
-        else:
-            cand, key = [(0, H, 0, W)], (lambda bd, u: True)
-        cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop bands no op reads
+        # cells of the grid spanned by the slices' row and column boundaries;
+        # keep the cells some slice reads
+        rcuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
+        ccuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
+        cand = [(r0, r1, c0, c1) for r0, r1 in zip(rcuts, rcuts[1:]) for c0, c1 in zip(ccuts, ccuts[1:])]
+
+        def key(bd, u):
+            return bd[0] < u[2] and u[1] < bd[1] and bd[2] < u[4] and u[3] < bd[3]
+
+        cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop cells no op reads
         if len(cand) > 16:
-            cand, key = [(0, H, 0, W)], (lambda bd, u: True)
+            cand = [(0, H, 0, W)]
         bands[j] = cand
         for u in sl:
             need[(u[0], j)] = [k for k, bd in enumerate(cand) if key(bd, u)]
