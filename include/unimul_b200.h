@@ -136,6 +136,11 @@ typedef struct {
   int32_t a_get, b_get;    /* um_gemm_acc_fused: 1 if this op's a / b operand is written by an
                               in-kernel get of the same launch (must then be TMA-aligned) */
   uint64_t get_mask;       /* bit i: the op starts loading only after gets[i] has landed  */
+  uint32_t* done_flag;     /* non-NULL: when every op of the launch sharing this flag has
+                              written all of its C tiles, the kernel adds the number of
+                              those ops to *done_flag (release, system scope; may be a
+                              peer / IPC-mapped word), so a consumer expecting n ops
+                              waits for *done_flag >= n whatever the launch split  */
 } um_gemm_op;
 
 /* A pull executed INSIDE the GEMM launch (um_gemm_acc_fused): src slice
@@ -148,6 +153,8 @@ typedef struct {
 
 /* Max pulls per fused launch. */
 #define UM_GEMM_MAX_GETS 64
+/* Max distinct done_flags per launch. */
+#define UM_GEMM_MAX_SIGNALS 64
 
 /* Ops per grouped launch that travel inside the kernel parameters; longer
  * lists are staged through a stream-ordered device allocation.            */
@@ -203,6 +210,11 @@ UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
 UM_API int um_signal(uint32_t* flag, uint32_t value, void* stream);
 /* 1 if um_signal is usable on `device` (stream memory operations), else 0. */
 UM_API int um_signal_supported(int32_t device, int32_t* out);
+/* Stream-ordered wait: work enqueued on `stream` after this call starts only
+ * once *flag >= value (32-bit, stream memory operation: no SM is held, so it
+ * cannot starve the kernel that will produce the value).  The consumer side
+ * of um_gemm_op.done_flag (K4 waiting for every replica's slice).          */
+UM_API int um_wait_geq(const uint32_t* flag, uint32_t value, void* stream);
 
 /* ======================================================================== */
 /* K3: one-sided accumulate (fabric.py:203-234, distmatrix.py:170-209)        */

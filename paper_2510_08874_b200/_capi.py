@@ -71,7 +71,7 @@ class UmGemmOp(ctypes.Structure):
     _fields_ = [("a", UmView), ("b", UmView), ("c", UmView),
                 ("c_remote", ctypes.c_int32), ("wait_value", ctypes.c_uint32),
                 ("wait_flag", ctypes.c_void_p), ("a_get", ctypes.c_int32), ("b_get", ctypes.c_int32),
-                ("get_mask", ctypes.c_uint64)]
+                ("get_mask", ctypes.c_uint64), ("done_flag", ctypes.c_void_p)]
 
 
 class UmGetDesc(ctypes.Structure):
@@ -100,6 +100,7 @@ _SIGS = {
     "um_get": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_signal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
     "um_signal_supported": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_int32)]),
+    "um_wait_geq": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
     "um_accumulate": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_void_p]),
     "um_copy": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),

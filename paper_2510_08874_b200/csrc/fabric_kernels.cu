@@ -235,6 +235,31 @@ static StreamWriteValue32Fn stream_write_fn() {
   return fn;
 }
 
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWaitValue32Fn stream_wait_fn() {
+  static StreamWaitValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitValue32Fn>(p);
+  });
+  return fn;
+}
+
+extern "C" int um_wait_geq(const uint32_t* flag, uint32_t value, void* stream) {
+  if (!flag) return fail(UM_EVALUE, "null flag");
+  if ((reinterpret_cast<uintptr_t>(flag) & 3) != 0) return fail(UM_EVALUE, "flag must be 4-byte aligned");
+  StreamWaitValue32Fn fn = stream_wait_fn();
+  if (!fn) return fail(UM_ECUDA, "cuStreamWaitValue32 unavailable");
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                  CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(UM_ECUDA, "cuStreamWaitValue32 failed (code " + std::to_string((int)r) + ")");
+  return UM_OK;
+}
+
 extern "C" int um_signal_supported(int32_t device, int32_t* out) {
   if (!out) return fail(UM_EVALUE, "null out pointer");
   (void)device;  // 32-bit stream memory operations are core functionality since CUDA 12

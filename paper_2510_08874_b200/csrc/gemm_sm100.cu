@@ -104,7 +104,7 @@ struct alignas(16) Work {
   float* c_ptr;
   const uint32_t* wait_flag;  // non-null: operands are staged by a get; wait for *wait_flag >= wait_value
   uint32_t wait_value;
-  int32_t pad_;
+  int32_t slot;               // completion-signal slot (-1: none)
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
 };
 
@@ -165,12 +165,25 @@ constexpr int TQ = 4;  // tile-queue depth (producer runs <= 3 tiles ahead of th
 constexpr int MAX_INLINE_OPS = UM_GEMM_MAX_INLINE_OPS;
 constexpr int MAX_GETS = UM_GEMM_MAX_GETS;
 constexpr int GET_CHUNK_BYTES = 32 * 1024;
+constexpr int MAX_SLOTS = UM_GEMM_MAX_SIGNALS;
+
+// Completion signal: once every tile of every op naming this slot has been
+// written (all epilogue warps of both CTAs of each tile arrive), the kernel
+// adds 1 to *flag with release semantics at system scope (flag may be a peer
+// or IPC-mapped word: the replica reducer on another GPU waits on it).
+struct alignas(16) SignalSlot {
+  uint32_t* flag;
+  int32_t expected;    // epilogue-warp arrivals (tiles x warps x CTAs) that complete the slot
+  uint32_t increment;  // added to *flag: the number of ops of this launch naming the flag
+};
 struct alignas(64) LaunchArgs {
   const Work* works;          // null: use inl_works
   const CUtensorMap* maps;    // null: use inl_maps
   int nwork, total_tiles;
   int* counters;              // per-stream {tile, done clusters, get chunk, get done[MAX_GETS]}
   int ngets, total_chunks;
+  int nslots, pad_;
+  SignalSlot slots[MAX_SLOTS];
   CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
   Work inl_works[MAX_INLINE_OPS];
   GetDesc gets[MAX_GETS];
@@ -234,6 +247,9 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
     else ptx::mbar_arrive_cluster(&tq_empty[slot], 0);
     return t;
   };
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int s = 0; s < args.nslots; ++s)   // a slot whose ops have no tile is complete at once
+      if (args.slots[s].expected == 0) ptx::red_release_sys_add_u32(args.slots[s].flag, args.slots[s].increment);
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
@@ -548,6 +564,21 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           }
         }
       }
+      if (wk.slot >= 0) {
+        // this warp's share of the tile is in C: complete its bulk writes, then
+        // count it; the last arrival of the slot publishes the signal
+        if (lane == 0) ptx::bulk_wait<0>();
+        ptx::fence_proxy_async_global();
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) {
+          const SignalSlot& sg = args.slots[wk.slot];
+          if (atomicAdd(&args.counters[3 + MAX_GETS + wk.slot], 1) == sg.expected - 1) {
+            __threadfence_system();
+            ptx::red_release_sys_add_u32(sg.flag, sg.increment);
+          }
+        }
+      }
     }
     if (lane == 0) ptx::bulk_wait<0>();
   } else if (args.ngets > 0) {
@@ -722,7 +753,7 @@ static int* stream_counters(int device, cudaStream_t stream) {
   for (auto& e : table)
     if (e.first.first == device && e.first.second == stream) return e.second;
   int* p = nullptr;
-  constexpr size_t bytes = (3 + MAX_GETS) * sizeof(int);
+  constexpr size_t bytes = (3 + MAX_GETS + MAX_SLOTS) * sizeof(int);
   if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
   // zero in stream order: torch's streams are non-blocking, so a plain
   // cudaMemset (legacy default stream) would race the first launch
@@ -810,7 +841,7 @@ struct StageCopy {
   size_t spitch, width, height;
 };
 struct Prepared {
-  int device = 0, CG = 2, NT = 256, EW = 4, ngets = 0;
+  int device = 0, CG = 2, NT = 256, EW = 4, ngets = 0, nslots = 0;
   bool persistent = false, empty = true;
   void* scratch = nullptr;    // aligned copies of misaligned operand slices
   void* dbuf = nullptr;       // work list + tensor maps of > MAX_INLINE_OPS ops
@@ -896,6 +927,26 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   works.reserve(nops);
   maps.reserve(3 * nops);
   int total = 0;
+  // completion-signal slots: one per distinct done_flag
+  std::vector<uint32_t*> slot_flags;
+  std::vector<int> slot_expected;
+  std::vector<uint32_t> slot_inc;
+  for (int i = 0; i < nops; ++i) {
+    uint32_t* f = ops[i].done_flag;
+    if (!f) continue;
+    auto it = std::find(slot_flags.begin(), slot_flags.end(), f);
+    if (it == slot_flags.end()) {
+      if ((reinterpret_cast<uintptr_t>(f) & 3) != 0) return fail(UM_EVALUE, "done_flag must be 4-byte aligned");
+      slot_flags.push_back(f);
+      slot_expected.push_back(0);
+      slot_inc.push_back(1);
+    } else {
+      ++slot_inc[it - slot_flags.begin()];
+    }
+  }
+  if ((int)slot_flags.size() > MAX_SLOTS)
+    return fail(UM_EVALUE, "more than " + std::to_string(MAX_SLOTS) + " distinct done_flags in one launch");
+  const int epi_arrivals = (CG == 2 ? 2 : 1) * ((CG == 2 && kn.epi_warps == 8) ? 8 : 4);
   for (int i = 0; i < nops; ++i) {
     const um_gemm_op& op = ops[i];
     if (op.c_remote && op.c.dtype == UM_F32 && (reinterpret_cast<uintptr_t>(op.c.base) & 3))
@@ -956,6 +1007,11 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
     total += w.tiles_m * w.tiles_n;
+    w.slot = -1;
+    if (op.done_flag) {
+      w.slot = (int)(std::find(slot_flags.begin(), slot_flags.end(), op.done_flag) - slot_flags.begin());
+      slot_expected[w.slot] += w.tiles_m * w.tiles_n * epi_arrivals;
+    }
     CUtensorMap ma, mbm, mc;
     if ((rc = encode_2d(&ma, op.a, BK, BM, "A")) || (rc = encode_2d(&mbm, op.b, 64, BK, "B"))) return rc;
     if (!op.c_remote) {
@@ -971,6 +1027,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   LaunchArgs& args = P->args;
   args.nwork = (int)works.size();
   args.total_tiles = total;
+  args.nslots = (int)slot_flags.size();
+  for (int s = 0; s < args.nslots; ++s) args.slots[s] = {slot_flags[s], slot_expected[s], slot_inc[s]};
   // ---- in-kernel gets (fused K2)
   int chunks = 0;
   for (int i = 0; i < ngets; ++i) {
@@ -999,7 +1057,10 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   args.ngets = ngets;
   args.total_chunks = chunks;
   P->ngets = ngets;
-  P->empty = total == 0 && ngets == 0;   // gets only: still one launch (get warps, no tiles)
+  P->nslots = args.nslots;
+  // gets only / signals only: still one launch (get warps; slots with no tile
+  // are signalled at kernel start)
+  P->empty = total == 0 && ngets == 0 && args.nslots == 0;
   void* dbuf = nullptr;
   if (works.size() <= (size_t)MAX_INLINE_OPS) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
@@ -1035,6 +1096,8 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   args.counters = stream_counters(P->device, stream);
   if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
   if (P->ngets) UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + P->ngets) * sizeof(int), stream));
+  if (P->nslots)
+    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 3 + MAX_GETS, 0, P->nslots * sizeof(int), stream));
   if (P->CG == 1) return launch<1, 256, 4>(args, P->device, stream);
   if (P->NT == 512)
     return P->EW == 8 ? launch<2, 512, 8>(args, P->device, stream) : launch<2, 512, 4>(args, P->device, stream);

@@ -290,6 +290,17 @@ class Fabric:
             self._streams[key] = s
         return s
 
+    def devices_shared_across_processes(self) -> bool:
+        """True when two processes of the world drive the same physical GPU
+        (e.g. several ranks on a one-GPU box).  Decided once, collectively."""
+        if self.world.size == 1 or self.placement_only:
+            return False
+        if not hasattr(self, "_shared_devs"):
+            uuid = str(torch.cuda.get_device_properties(self.devices[0]).uuid)
+            ids = self.world.all_gather_object(uuid)
+            self._shared_devs = len(set(ids)) < len(ids)
+        return self._shared_devs
+
     def _require_data(self):
         if self.placement_only:
             raise RuntimeError("placement-only fabric (no CUDA device): data movement is unavailable")

@@ -30,6 +30,7 @@ return, so torch code sees the results without host synchronisation.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -70,6 +71,13 @@ class ExecConfig:
                          MiB: each sub-op starts when its band has landed.
       k_split            > 1: split such ops along k instead (one A and one B
                          slab per sub-op, one extra C read-modify-write each).
+      overlap_reduce     replicated C under Stationary C: each C tile is cut
+                         into c * reduce_panels row sub-slices; the K1
+                         epilogue signals every finished sub-slice to its
+                         reducer (done_flag), whose K4 starts on a stream wait
+                         (um_wait_geq) while the GEMMs go on — no run-level
+                         barrier between the GEMMs and the reduction.
+      reduce_panels      sub-slices per replica and tile (>= 1).
       get_engine         "kernel": remote slices are pulled by get warps INSIDE
                          the K1 launch (um_gemm_acc_fused) and each op starts
                          when its pulls have landed — one launch per rank (up
@@ -92,6 +100,8 @@ class ExecConfig:
     reduce_distributed: bool = True
     get_engine: str = "kernel"
     mn_split: int = 4
+    overlap_reduce: bool = True
+    reduce_panels: int = 2
     k_split: int = 0
 
     def __post_init__(self):
@@ -107,6 +117,8 @@ class ExecConfig:
             raise ValueError(f"unknown get_engine {self.get_engine!r}")
         if self.k_split < 0 or self.mn_split < 0:
             raise ValueError("k_split / mn_split must be >= 0")
+        if self.reduce_panels < 1:
+            raise ValueError("reduce_panels must be >= 1")
         if self.gemm_batch < 0:
             raise ValueError("gemm_batch must be >= 0")
 
@@ -350,7 +362,7 @@ def _tma_ok(v) -> bool:
     return (v.col_lo * es) % 16 == 0 and (v.pitch * es) % 16 == 0 and (v.base or 0) % 16 == 0
 
 
-def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig):
+def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: dict | None = None):
     """Host-only planning of a rank's in-kernel pulls (no device work).
 
     Returns (items, bands, need):
@@ -361,6 +373,9 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig):
              along the dimension in which the (sub-)ops' slices differ, bands
              no op reads dropped (None for copy-engine fetches);
       need   (item, fetch) -> indices of the bands the item reads.
+    row_cuts   op -> cut positions along its m range (relative): the op is split
+             exactly there and nowhere else (overlapped replica reduction:
+             every item then lies in one reduction sub-slice of its C tile).
     """
     nf = len(s.fetches)
     # Sub-ops: an op that must first pull a large amount (cfg4: whole 8192^2
@@ -389,6 +404,11 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig):
         pb = pulled(i, s.b_src[i]) if s.b_src[i] != s.a_src[i] else 0
         unfused_remote = s.c_remote[i] and not cfg.fused_accumulate
         nsub, dim = 1, None
+        if row_cuts is not None and i in row_cuts:
+            cuts_i = sorted({0, mlen} | {c for c in row_cuts[i] if 0 < c < mlen})
+            for t in range(len(cuts_i) - 1):
+                items.append((i, t, cuts_i[t], cuts_i[t + 1], 0, nlen, 0, klen))
+            continue
         if not unfused_remote and pa + pb >= _SPLIT_BYTES:
             if cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
                 nsub, dim = int(min(cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
@@ -481,6 +501,8 @@ class _RankRun:
         self.stats = RunStats()
         self.buffers = []
         self.done = None
+        self.signals = None        # op -> (row cuts, (m0, m1) -> done_flag): overlapped replica reduction
+        self.signals_key = None
         for ev in start_events:
             self.gs.wait_event(ev)
             self.cs.wait_event(ev)
@@ -491,7 +513,7 @@ class _RankRun:
     def issue(self):
         """Replay this rank's issue plan (built once per schedule and knob set)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
-               self.cfg.k_split, self.cfg.mn_split, _SPLIT_BYTES, _SPLIT_MIN)
+               self.cfg.k_split, self.cfg.mn_split, _SPLIT_BYTES, _SPLIT_MIN, self.signals_key)
         plans = self.sched.__dict__.setdefault("plans", {})
         plan = plans.get(key)
         if plan is None:
@@ -537,7 +559,9 @@ class _RankRun:
                                um_dtype(staged[j].dtype), self.dev)
             return src, dst
 
-        items, bands, need = plan_bands(s, in_kernel, self.cfg)
+        items, bands, need = plan_bands(s, in_kernel, self.cfg,
+                                        None if self.signals is None else {i: cuts for i, (cuts, _) in
+                                                                           self.signals.items()})
 
         for j, f in enumerate(s.fetches):
             if not in_kernel[j]:
@@ -633,6 +657,8 @@ class _RankRun:
             g.a_get = int(s.a_src[i] >= 0 and in_kernel[s.a_src[i]])
             g.b_get = int(s.b_src[i] >= 0 and in_kernel[s.b_src[i]])
             g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot)
+            if self.signals is not None and i in self.signals:
+                g.done_flag = self.signals[i][1](m0, m1)
             batch.append(g)
             batch_remote += int(remote)
         flush()
@@ -924,6 +950,129 @@ def _cross_process(A, B, C, cfg: ExecConfig) -> bool:
     return cross
 
 
+class _ReduceOverlap:
+    """Replica reduction overlapped with the GEMMs (replicated C, Stationary C).
+
+    Every C tile is cut into c * panels row sub-slices (multiples of 256 rows,
+    the K1 tile height); sub-slice k is reduced by the owner of replica
+    k mod c (the distributed K4 of reduce_replicas, at finer grain, so every
+    reducer's work arrives spread over the GEMM).  Each rank's ops are split at
+    the sub-slice rows and carry a done_flag pointing at a word on the
+    sub-slice's reducer (symmetric heap: a peer or IPC-mapped address); the K1
+    epilogue adds the number of finished ops there (release, system scope).
+    The reducer's stream waits (um_wait_geq, a stream memory operation, no SM
+    held) for every contributing op of every replica in this run, then runs
+    K4 for the sub-slice.  Flags only grow: run e waits for e * expected.
+    """
+
+    def __init__(self, A, B, C, cfg: ExecConfig):
+        fab = C.fabric
+        p, c = fab.nprocs, C.c
+        self.C = C
+        self.subs = {}
+        n = c * cfg.reduce_panels
+        for t in C.grid.tiles():
+            rows = len(C.tile_bounds(t).rows)
+            cuts = sorted({0, rows} | {rows * s // n // 256 * 256 for s in range(1, n)})
+            self.subs[t] = [(cuts[k], cuts[k + 1], k % c) for k in range(len(cuts) - 1)]
+        counts = [0] * p
+        self.word = {}
+        for t, lst in self.subs.items():
+            for k, (_, _, rep) in enumerate(lst):
+                red = C.owner_rank(t, rep)
+                self.word[(t, k)] = (red, counts[red])
+                counts[red] += 1
+        # flag words live in the symmetric heap (same allocation order on every process)
+        self.flag_segs = [fab.alloc_tile(r, 1, max(1, counts[r]), torch.float32) for r in range(p)]
+        for seg in self.flag_segs:
+            if seg.storage is not None:
+                with torch.cuda.device(seg.device):
+                    seg.storage.zero_()
+        fab.heap.exchange()
+        # ops contributing to each sub-slice, over every replica's owner (host-only planning)
+        self.expected = {}
+        for r in range(p):
+            for op in lower_direct(A, B, C, cfg, r).ops:
+                lo, hi = op.c_local.rows.lo, op.c_local.rows.hi
+                for k, (r0, r1, _) in enumerate(self.subs[op.c_tile]):
+                    if lo < r1 and r0 < hi:
+                        self.expected[(op.c_tile, k)] = self.expected.get((op.c_tile, k), 0) + 1
+        self.epoch = 0
+        if fab.world.size > 1:
+            fab.synchronize()        # zeroed flags in place before any process can signal
+
+    def flag_ptr(self, t, k) -> int:
+        red, idx = self.word[(t, k)]
+        return self.flag_segs[red].ptr + 4 * idx
+
+    def signals_for(self, sched: DirectSchedule) -> dict:
+        sig = {}
+        for i, op in enumerate(sched.ops):
+            t, lo, hi = op.c_tile, op.c_local.rows.lo, op.c_local.rows.hi
+            cuts = [r0 - lo for r0, _, _ in self.subs[t] if lo < r0 < hi]
+
+            def flag(m0, m1, t=t, lo=lo):
+                row = lo + m0
+                for k, (r0, r1, _) in enumerate(self.subs[t]):
+                    if r0 <= row < r1:
+                        return self.flag_ptr(t, k)
+                raise AssertionError("item outside its C tile")
+
+            sig[i] = (cuts, flag)
+        return sig
+
+    def reduce(self, start_events) -> list:
+        """Enqueue wait + K4 per sub-slice on the reducers' streams; return done events."""
+        C, fab = self.C, self.C.fabric
+        lib = _capi.load()
+        self.epoch += 1
+        done = []
+        for t, lst in self.subs.items():
+            dst = C.segment(t, 0)
+            if dst.length == 0:
+                continue
+            srcs = [C.segment(t, r) for r in range(1, C.c)]
+            for k, (r0, r1, rep) in enumerate(lst):
+                red = C.owner_rank(t, rep)
+                if not fab.is_local(red) or r1 <= r0:
+                    continue
+                dev = fab.device_of(red)
+                stream = fab.stream(red, "reduce")
+                for ev in start_events:
+                    stream.wait_event(ev)
+                sp = ctypes.c_void_p(stream.cuda_stream)
+                exp = self.expected.get((t, k), 0)
+                with torch.cuda.device(dev):
+                    if exp:
+                        _capi.check(lib.um_wait_geq(ctypes.c_void_p(self.flag_ptr(t, k)),
+                                                    (self.epoch * exp) & 0xFFFFFFFF, sp), "um_wait_geq")
+                    dv = dst.um_view(r0, r1, 0, dst.cols)
+                    sv = (_capi.UmView * len(srcs))(*[s_.um_view(r0, r1, 0, s_.cols) for s_ in srcs])
+                    _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), sp), "um_reduce_replicas")
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                done.append(ev)
+        return done
+
+
+def _overlap_for(A, B, C, cfg: ExecConfig):
+    if not (cfg.overlap_reduce and cfg.reduce_distributed and C.c > 1
+            and cfg.stationarity is Stationarity.STATIONARY_C):
+        return None
+    # processes time-sharing one GPU (no MPS) could park a stream wait that only
+    # another process's kernel can satisfy: keep the barrier + K4 path there
+    if C.fabric.devices_shared_across_processes() and os.environ.get("UM_OVERLAP_SHARED") != "1":
+        return None
+    key = ("ovl", id(A), id(B), cfg.reduce_panels, cfg.staging, cfg.same_device_gets)
+    cache = C.__dict__.setdefault("_ovl_cache", {})
+    hit = cache.get(key)
+    if hit is not None and hit[0] is A and hit[1] is B:
+        return hit[2]
+    ovl = _ReduceOverlap(A, B, C, cfg)
+    cache[key] = (A, B, ovl)
+    return ovl
+
+
 def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                      execution: str = "direct", machine=None, max_compute: int | None = None,
                      max_comm: int | None = None, threaded: bool = False) -> dict[int, RunStats]:
@@ -941,6 +1090,7 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
     ranks = fab.local_ranks()
     results: dict[int, RunStats] = {}
     cross = _cross_process(A, B, C, cfg) if execution == "direct" else fab.world.size > 1
+    ovl = _overlap_for(A, B, C, cfg) if execution == "direct" else None
     if cross:
         fab.synchronize()            # owners' pending writes visible before any remote pull
     start = _current_events(fab)
@@ -950,7 +1100,10 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
         for r in ranks:
             sched = lower_direct(A, B, C, cfg, r)
             _count_reference_traffic(A, B, C, cfg, sched)
-            runs.append(_RankRun(A, B, C, cfg, sched, start).issue())
+            run = _RankRun(A, B, C, cfg, sched, start)
+            if ovl is not None:
+                run.signals, run.signals_key = ovl.signals_for(sched), ("ovl", id(ovl))
+            runs.append(run.issue())
         for run in runs:
             run.stats.flops = int(fab.counters.flops[run.caller])
             results[run.caller] = run.stats
@@ -968,10 +1121,17 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
                 prog = lowering.lower_exhaustive(g, machine, max_compute, max_comm)
             results[r] = run_ir(prog, g, A, B, C, cfg, r)
         done = _current_events(fab)
-    if cross:
+    if ovl is not None:
+        # K4 per sub-slice, each started by its replicas' completion signals
+        # (no run-level barrier between the GEMMs and the reduction)
+        _join_current(fab, ovl.reduce(start) + done)
+        if fab.world.size > 1:
+            fab.synchronize()
+    elif cross:
         fab.synchronize()            # run-level barrier across processes
-    if C.c > 1:
+    if C.c > 1 and ovl is None:
         reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done)
+    if C.c > 1:
         for t in C.grid.tiles():      # reference-model accounting of the pulls
             dst = C.segment(t, 0)
             for r in range(1, C.c):
