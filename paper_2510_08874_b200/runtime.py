@@ -693,6 +693,11 @@ class _RankRun:
                     self._scratch_gemm(*act[1:])
             for j in plan.final_waits:
                 self.cs.wait_event(events[j])
+            # join the get stream back even when it carried nothing (keeps the
+            # multiply capturable into a CUDA graph: no unjoined forked stream)
+            ev = torch.cuda.Event()
+            ev.record(self.gs)
+            self.cs.wait_event(ev)
             self.done = torch.cuda.Event()
             self.done.record(self.cs)
         fab.counters.merge(plan.traffic)
