@@ -165,7 +165,10 @@ UM_API int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, voi
 
 /* Grouped persistent launch over a list of ops on one device.  All ops'
  * operands must be readable from `device`.  Equivalent to calling
- * um_gemm_acc for each op in order (accumulates commute).                  */
+ * um_gemm_acc for each op in order (accumulates commute).  Ops whose C views
+ * are identical (same base, slice, pitch and epilogue) form a k-chain: their
+ * products are accumulated in TMEM in list order and each output tile is
+ * reduced into C once (UM_GEMM_CHAIN=0 turns this off).                    */
 UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream);
 
 /* Fused get -> GEMM: ONE persistent launch that pulls `gets` with dedicated

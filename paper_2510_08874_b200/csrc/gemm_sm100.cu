@@ -100,6 +100,8 @@ struct alignas(16) Work {
   int32_t a_pol, b_pol;     // L2 policy: 0 normal, 1 evict_first, 2 evict_last
   int32_t c_pol, prefetch;  // L2 policy of the C reduce-add (-1: no hint); L2 prefetch distance (k-blocks)
   int32_t sched_static, no_end_stagger;  // profiling A/B knobs: static round-robin tiles; no end stagger
+  int32_t nseg, seg_kb;     // k-chain: head has nseg segments (itself + nseg-1 continuations that follow
+                            // it in the work list, same C region); seg_kb = k-blocks of this segment
   int64_t c_pitch;
   float* c_ptr;
   const uint32_t* wait_flag;  // non-null: operands are staged by a get; wait for *wait_flag >= wait_value
@@ -262,7 +264,8 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
       const uint64_t pols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
       int stage = 0;
       uint32_t phase = 0;
-      int ready_work = -1;   // highest work index whose get-arrival flag has been observed
+      uint64_t landed = 0;   // in-kernel gets whose every chunk this producer has observed
+      int flag_ok = -1;      // highest work index whose external arrival flag has been observed
       for (int i = 0;; ++i) {
         int t;
         if (leader) {
@@ -295,23 +298,27 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           }
           break;
         }
-        const int w = find_work(works, nwork, t);
+        const int w0 = find_work(works, nwork, t);
+        int mb, nb;
+        tile_coords(works[w0], t - works[w0].tile_start, mb, nb);
+        // a k-chain: the segments (ops with the same C region) are loaded one
+        // after the other into the same accumulator, one epilogue per tile
+        for (int w = w0; w < w0 + works[w0].nseg; ++w) {
         const Work& wk = works[w];
-        if (w > ready_work) {
-          // fused get -> GEMM: this op reads operand slices a get is still
-          // delivering; wait until every chunk of those gets has landed
-          if (wk.wait_flag) ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
-          for (uint64_t msk = wk.wait_mask; msk; msk &= msk - 1) {
-            const int gi = __ffsll((long long)msk) - 1;
-            ptx::wait_count_geq(&args.counters[3 + gi], args.gets[gi].nchunks);
-          }
-          ready_work = w;
+        // fused get -> GEMM: this segment reads operand slices a get is still
+        // delivering; wait until every chunk of those gets has landed
+        if (wk.wait_flag && w > flag_ok) {
+          ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
+          flag_ok = w;
         }
+        for (uint64_t msk = wk.wait_mask & ~landed; msk; msk &= msk - 1) {
+          const int gi = __ffsll((long long)msk) - 1;
+          ptx::wait_count_geq(&args.counters[3 + gi], args.gets[gi].nchunks);
+        }
+        landed |= wk.wait_mask;
         const CUtensorMap* ma = &maps[3 * w + 0];
         const CUtensorMap* mbm = &maps[3 * w + 1];
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
-        int mb, nb;
-        tile_coords(wk, t - wk.tile_start, mb, nb);
         const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
@@ -325,9 +332,9 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
               ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, wk.b_row0 + kb * BK);
         };
         const int pf = wk.prefetch;
-        for (int kb = 0; kb < min(pf, wk.num_kb); ++kb) prefetch(kb);
-        for (int kb = 0; kb < wk.num_kb; ++kb) {
-          if (pf > 0 && kb + pf < wk.num_kb) prefetch(kb + pf);
+        for (int kb = 0; kb < min(pf, wk.seg_kb); ++kb) prefetch(kb);
+        for (int kb = 0; kb < wk.seg_kb; ++kb) {
+          if (pf > 0 && kb + pf < wk.seg_kb) prefetch(kb + pf);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
@@ -350,6 +357,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
             }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        }  // k-chain segments
       }
     }
   } else if (warp == 1) {
@@ -724,6 +732,7 @@ static int env_int(const char* name, int dflt) {
 struct Knobs {
   int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 0, sched_static = 0;
   int epi_warps = 4;
+  int chain = 1;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -739,6 +748,7 @@ static const Knobs& knobs() {
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
+    k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
   });
   return k;
 }
@@ -973,6 +983,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.tiles_m = (int32_t)((m + BM * CG - 1) / (BM * CG));
     w.tiles_n = (int32_t)((n + NT - 1) / NT);
     w.num_kb = (int32_t)((k + BK - 1) / BK);
+    w.seg_kb = w.num_kb;
+    w.nseg = 1;
     w.tile_start = total;
     w.c_remote = op.c_remote;
     if (!op.c_remote) {
@@ -1008,10 +1020,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
     total += w.tiles_m * w.tiles_n;
     w.slot = -1;
-    if (op.done_flag) {
+    if (op.done_flag)
       w.slot = (int)(std::find(slot_flags.begin(), slot_flags.end(), op.done_flag) - slot_flags.begin());
-      slot_expected[w.slot] += w.tiles_m * w.tiles_n * epi_arrivals;
-    }
     CUtensorMap ma, mbm, mc;
     if ((rc = encode_2d(&ma, op.a, BK, BM, "A")) || (rc = encode_2d(&mbm, op.b, 64, BK, "B"))) return rc;
     if (!op.c_remote) {
@@ -1024,6 +1034,50 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     maps.push_back(mbm);
     maps.push_back(mc);
   }
+  // ---- k-chains: ops writing the same C region (Stationary C: the k-chunks of
+  // one C tile) become one work whose segments accumulate in TMEM, so each
+  // output tile is drained and reduced into C once instead of once per op
+  if (kn.chain && works.size() > 1) {
+    auto same_c = [](const Work& x, const Work& y) {
+      return x.c_ptr == y.c_ptr && x.c_row0 == y.c_row0 && x.c_col0 == y.c_col0 && x.m == y.m && x.n == y.n &&
+             x.c_pitch == y.c_pitch && x.c_remote == y.c_remote && x.slot == y.slot && x.c_pol == y.c_pol;
+    };
+    std::vector<Work> cw;
+    std::vector<CUtensorMap> cm;
+    std::vector<char> used(works.size(), 0);
+    int tot = 0;
+    for (size_t i = 0; i < works.size(); ++i) {
+      if (used[i]) continue;
+      std::vector<size_t> grp = {i};
+      for (size_t j = i + 1; j < works.size(); ++j)
+        if (!used[j] && same_c(works[i], works[j])) grp.push_back(j);
+      int kb = 0;
+      for (size_t g : grp) {
+        used[g] = 1;
+        kb += works[g].seg_kb;
+      }
+      Work head = works[i];
+      head.nseg = (int32_t)grp.size();
+      head.num_kb = kb;
+      head.tile_start = tot;
+      tot += head.tiles_m * head.tiles_n;
+      cw.push_back(head);
+      for (int q = 0; q < 3; ++q) cm.push_back(maps[3 * i + q]);
+      for (size_t g = 1; g < grp.size(); ++g) {
+        Work c = works[grp[g]];
+        c.nseg = 0;
+        c.tile_start = tot;       // continuation: never the target of a tile index
+        cw.push_back(c);
+        for (int q = 0; q < 3; ++q) cm.push_back(maps[3 * grp[g] + q]);
+      }
+    }
+    works.swap(cw);
+    maps.swap(cm);
+    total = tot;
+  }
+  // completion-signal arrivals: every epilogue warp of both CTAs, once per tile of each work head
+  for (const Work& w : works)
+    if (w.nseg > 0 && w.slot >= 0) slot_expected[w.slot] += w.tiles_m * w.tiles_n * epi_arrivals;
   LaunchArgs& args = P->args;
   args.nwork = (int)works.size();
   args.total_tiles = total;

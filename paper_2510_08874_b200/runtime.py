@@ -78,6 +78,9 @@ class ExecConfig:
                          (um_wait_geq) while the GEMMs go on — no run-level
                          barrier between the GEMMs and the reduction.
       reduce_panels      sub-slices per replica and tile (>= 1).
+      chain_order        issue ops that write the same C region back to back
+                         (K1 accumulates such a k-chain in TMEM and reduces
+                         into C once per tile).
       get_engine         "kernel": remote slices are pulled by get warps INSIDE
                          the K1 launch (um_gemm_acc_fused) and each op starts
                          when its pulls have landed — one launch per rank (up
@@ -101,6 +104,7 @@ class ExecConfig:
     get_engine: str = "kernel"
     mn_split: int = 4
     overlap_reduce: bool = True
+    chain_order: bool = True
     reduce_panels: int = 2
     k_split: int = 0
 
@@ -425,6 +429,21 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: di
             kk = (lo, hi) if dim == "k" else (0, klen)
             items.append((i, t, *mm, *nn, *kk))
 
+    # device order: items writing the same C region run back to back (K1 chains
+    # them into one accumulator: one epilogue per tile), groups in order of first
+    # appearance; the pulls then arrive in the order those chains need them.
+    # (RunStats keep the reference's execution order: this is device-internal.)
+    if cfg.chain_order:
+        def ckey(it):
+            i, t, m0, m1, n0, n1, k0, k1 = it
+            cl = s.ops[i].c_local
+            return (s.ops[i].c_tile, cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
+
+        first = {}
+        for pos, it in enumerate(items):
+            first.setdefault(ckey(it), pos)
+        items = sorted(items, key=lambda it: first[ckey(it)])      # stable: k order kept inside a chain
+
     # in-kernel pulls are cut into bands along the dimension in which the
     # (sub-)ops' slices differ, so an op waits only for the slab it reads
     # (cfg5: a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
@@ -513,7 +532,7 @@ class _RankRun:
     def issue(self):
         """Replay this rank's issue plan (built once per schedule and knob set)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
-               self.cfg.k_split, self.cfg.mn_split, _SPLIT_BYTES, _SPLIT_MIN, self.signals_key)
+               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _SPLIT_BYTES, _SPLIT_MIN, self.signals_key)
         plans = self.sched.__dict__.setdefault("plans", {})
         plan = plans.get(key)
         if plan is None:
@@ -633,10 +652,6 @@ class _RankRun:
                                   ga.dtype, ga.device)
                 gb = _capi.UmView(gb.base, gb.row_lo + k0, gb.row_lo + k1, gb.col_lo + n0, gb.col_lo + n1, gb.pitch,
                                   gb.dtype, gb.device)
-            if t == 0:
-                st.executed_ops.append(op)
-                st.a_requests.append(op.a_tile)
-                st.b_requests.append(op.b_tile)
             if remote and not self.cfg.fused_accumulate:
                 # unfused remote update (scratch GEMM + K3): its pulls must have landed
                 flush()
@@ -662,6 +677,11 @@ class _RankRun:
             batch.append(g)
             batch_remote += int(remote)
         flush()
+        # RunStats report the reference's execution order (runtime.py:213-236),
+        # whatever order the device runs the (sub-)ops in
+        st.executed_ops = list(s.ops)
+        st.a_requests = [op.a_tile for op in s.ops]
+        st.b_requests = [op.b_tile for op in s.ops]
         plan.final_waits = [j for j in range(nf) if not in_kernel[j] and not waited[j]]
         st.peak_inflight_gemms = 1 if s.ops else 0
         return plan
