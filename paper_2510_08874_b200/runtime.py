@@ -1026,6 +1026,13 @@ class _ReduceOverlap:
         if fab.world.size > 1:
             fab.synchronize()        # zeroed flags in place before any process can signal
 
+    def sub_slice_of(self, t, row: int) -> int:
+        """Index of the sub-slice of C tile t holding tile-local `row`."""
+        for k, (r0, r1, _) in enumerate(self.subs[t]):
+            if r0 <= row < r1:
+                return k
+        raise AssertionError("row outside its C tile")
+
     def flag_ptr(self, t, k) -> int:
         red, idx = self.word[(t, k)]
         return self.flag_segs[red].ptr + 4 * idx
@@ -1037,11 +1044,7 @@ class _ReduceOverlap:
             cuts = [r0 - lo for r0, _, _ in self.subs[t] if lo < r0 < hi]
 
             def flag(m0, m1, t=t, lo=lo):
-                row = lo + m0
-                for k, (r0, r1, _) in enumerate(self.subs[t]):
-                    if r0 <= row < r1:
-                        return self.flag_ptr(t, k)
-                raise AssertionError("item outside its C tile")
+                return self.flag_ptr(t, self.sub_slice_of(t, lo + m0))
 
             sig[i] = (cuts, flag)
         return sig
