@@ -239,6 +239,7 @@ def b200_arm(args):
     import torch.distributed as dist
 
     from paper_2510_08874_b200 import ExecConfig, execute_multiply
+    from paper_2510_08874_b200 import engine as eng
     from paper_2510_08874_b200 import runtime as rt
     from paper_2510_08874_b200.cli import build_problem
 
@@ -279,8 +280,8 @@ def b200_arm(args):
     for _ in range(args.warmup):
         execute_multiply(A, B, C, cfg)
     barrier()
-    rt.TRACE.clear()
-    rt.TRACE_ENABLED = True
+    eng.TRACE.clear()
+    eng.TRACE_ENABLED = True
     sampler = ClockSampler(local)
     barrier()
     sampler.start()
@@ -293,12 +294,12 @@ def b200_arm(args):
     e1.record()
     barrier()
     clocks = sampler.stop()
-    rt.TRACE_ENABLED = False
+    eng.TRACE_ENABLED = False
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     value = flops / (ms * 1e-3) / 1e12
     # dominant kernel (K1 grouped launch) durations, measured on its own stream
-    durs = [s.elapsed_time(e) for s, e, _ in rt.TRACE]
-    kflops = [f for _, _, f in rt.TRACE]
+    durs = [s.elapsed_time(e) for s, e, _ in eng.TRACE]
+    kflops = [f for _, _, f in eng.TRACE]
     peak, peak_sus, peak_kind = load_peaks()
     if durs:
         achieved = sum(kflops) / (sum(durs) * 1e-3) / 1e12

@@ -1,0 +1,312 @@
+"""Device issue of one rank's direct schedule: issue plans and their replay.
+
+A plan (built once per schedule and knob set) holds the persistent staging
+pool, the copy-engine pulls, and one prepared K1 launch per group
+(um_gemm_prepare) carrying the in-kernel pulls; every multiply replays it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from paper_2510_08874_b200 import _capi
+from paper_2510_08874_b200 import schedule as _sch
+from paper_2510_08874_b200.config import ExecConfig, RunStats
+from paper_2510_08874_b200.fabric import pitch_for, um_dtype
+from paper_2510_08874_b200.schedule import DirectSchedule, _tma_ok, plan_bands
+
+# Launch tracing for the benchmark's roofline: (start, end, algorithmic flops)
+# CUDA events recorded on the compute stream around every grouped K1 launch.
+TRACE: list = []
+TRACE_ENABLED = False
+
+
+def _current_events(fabric) -> list:
+    evs = []
+    for d in sorted({fabric.device_of(r) for r in fabric.local_ranks()}):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(d))
+        evs.append(ev)
+    return evs
+
+
+def _join_current(fabric, events):
+    for d in sorted({fabric.device_of(r) for r in fabric.local_ranks()}):
+        cur = torch.cuda.current_stream(d)
+        for ev in events:
+            cur.wait_event(ev)
+
+
+class _IssuePlan:
+    """One rank's issue plan: persistent staging buffers, copy-engine pulls,
+    and an action list of prepared K1 launches / stream waits / unfused
+    scratch updates, replayed by every multiply with the same schedule."""
+
+    def __init__(self, nprocs: int):
+        from paper_2510_08874_b200.fabric import FabricCounters
+
+        self.staged: list = []
+        self.host_fetches: list = []      # (fetch index, src view, dst view)
+        self.actions: list = []           # ("launch", handle, flops) | ("wait", j) | ("scratch", op, ga, gb)
+        self.final_waits: list = []
+        self.handles: list = []
+        self.traffic = FabricCounters(nprocs)   # wire bytes of the pulls, added per run
+        self.stats = RunStats()
+
+    def __del__(self):
+        try:
+            lib = _capi.load()
+            for h in self.handles:
+                lib.um_gemm_destroy(ctypes.c_void_p(h))
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class _RankRun:
+    """Device work of one rank's direct schedule (issued asynchronously)."""
+
+    def __init__(self, A, B, C, cfg: ExecConfig, sched: DirectSchedule, start_events):
+        self.A, self.B, self.C, self.cfg, self.sched = A, B, C, cfg, sched
+        fab = A.fabric
+        self.fab = fab
+        self.caller = sched.caller
+        self.dev = fab.device_of(self.caller)
+        self.gs = fab.stream(self.caller, "get")
+        self.cs = fab.stream(self.caller, "compute")
+        self.stats = RunStats()
+        self.buffers = []
+        self.done = None
+        self.signals = None        # op -> (row cuts, (m0, m1) -> done_flag): overlapped replica reduction
+        self.signals_key = None
+        for ev in start_events:
+            self.gs.wait_event(ev)
+            self.cs.wait_event(ev)
+
+    def _mat(self, name):
+        return self.A if name == "A" else self.B
+
+    def issue(self):
+        """Replay this rank's issue plan (built once per schedule and knob set)."""
+        key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
+               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key)
+        plans = self.sched.__dict__.setdefault("plans", {})
+        plan = plans.get(key)
+        if plan is None:
+            plan = plans[key] = self._build_plan()
+        self._replay(plan)
+        return self
+
+    def _build_plan(self) -> "_IssuePlan":
+        """Resolve everything host-side once: persistent staging buffers (the
+        paper's pre-allocated pool), which pulls run inside
+        the GEMM launch and which on the copy engines, the launch split, and one
+        prepared K1 launch (um_gemm_prepare) per group."""
+        lib = _capi.load()
+        s, fab = self.sched, self.fab
+        nf = len(s.fetches)
+        plan = _IssuePlan(fab.counters.nprocs)
+        st = plan.stats
+        with torch.cuda.device(self.dev):
+            for f in s.fetches:
+                M = self._mat(f.mat)
+                with torch.cuda.stream(self.cs):
+                    buf = torch.empty((f.r1 - f.r0, pitch_for(f.c1 - f.c0, M.dtype)), dtype=M.dtype,
+                                      device=f"cuda:{self.dev}")
+                buf.record_stream(self.gs)
+                plan.staged.append(buf)
+        staged = plan.staged
+        views = [(self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged),
+                  self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)) for i, op in enumerate(s.ops)]
+        # which pulls run inside the K1 launch: every op reading the staged slice
+        # must see a TMA-readable view of it (16-byte column start); the rest go
+        # through the copy engines with host-side ordering
+        in_kernel = [self.cfg.get_engine == "kernel"] * nf
+        for i in range(len(s.ops)):
+            for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
+                if src >= 0 and not _tma_ok(v):
+                    in_kernel[src] = False
+
+        def fetch_views(j, band=None):
+            f = s.fetches[j]
+            br0, br1, bc0, bc1 = band if band is not None else (0, f.r1 - f.r0, 0, f.c1 - f.c0)
+            src = self._mat(f.mat).segment(f.tile, f.replica).um_view(f.r0 + br0, f.r0 + br1, f.c0 + bc0, f.c0 + bc1)
+            dst = _capi.UmView(staged[j].data_ptr(), br0, br1, bc0, bc1, staged[j].stride(0),
+                               um_dtype(staged[j].dtype), self.dev)
+            return src, dst
+
+        items, bands, need = plan_bands(s, in_kernel, self.cfg,
+                                        None if self.signals is None else {i: cuts for i, (cuts, _) in
+                                                                           self.signals.items()})
+
+        for j, f in enumerate(s.fetches):
+            if not in_kernel[j]:
+                plan.host_fetches.append((j, *fetch_views(j)))
+                nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
+            else:
+                nbytes = sum((r1 - r0) * (c1 - c0) for r0, r1, c0, c1 in bands[j]) * staged[j].element_size()
+            plan.traffic.add_traffic(self.caller, f.owner, 0, 0, nbytes)
+            st.gets += 1
+            st.staged_bytes += nbytes
+        st.pool_acquired = st.pool_released = st.pool_peak = nf
+
+        # ---- K1 launch groups.  In-kernel pulls (bands) travel with the first
+        # launch that needs them; a copy-engine pull not yet waited on splits
+        # the group (the compute stream waits for its event).
+        batch: list = []
+        batch_gets: list = []            # (fetch, band) units of this launch, in first-use order
+        gets_slot: dict = {}             # unit -> 0-based slot in batch_gets
+        launched: set = set()
+        batch_remote = 0
+        waited = [False] * nf
+        cap = self.cfg.gemm_batch or _capi.GEMM_MAX_INLINE_OPS
+
+        def flush():
+            nonlocal batch, batch_remote, batch_gets, gets_slot
+            if not batch and not batch_gets:
+                return
+            arr = (_capi.UmGemmOp * max(1, len(batch)))(*batch)
+            garr = (_capi.UmGetDesc * max(1, len(batch_gets)))()
+            for gi, (j, k) in enumerate(batch_gets):
+                garr[gi].src, garr[gi].dst = fetch_views(j, bands[j][k])
+                launched.add((j, k))
+            h = ctypes.c_void_p()
+            _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, len(batch_gets), self.dev, ctypes.byref(h)),
+                        "um_gemm_prepare")
+            plan.handles.append(h.value)
+            flops = float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo) * (g.b.col_hi - g.b.col_lo)
+                              for g in batch))
+            plan.actions.append(("launch", h.value, flops))
+            st.launches += 1
+            st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
+            st.peak_inflight_accums = max(st.peak_inflight_accums, batch_remote)
+            batch, batch_remote, batch_gets, gets_slot = [], 0, [], {}
+
+        def host_wait(j):
+            if not waited[j]:
+                flush()
+                plan.actions.append(("wait", j))
+                waited[j] = True
+
+        for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
+            op = s.ops[i]
+            srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
+            for j in srcs:
+                if not in_kernel[j]:
+                    host_wait(j)
+            remote = s.c_remote[i] and self.fab.device_of(
+                self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
+            units = [(j, k) for j in dict.fromkeys(srcs) if in_kernel[j] for k in need[(it, j)]]
+            new_units = [u for u in units if u not in launched and u not in gets_slot]
+            if (len(batch) >= cap or (remote and batch_remote >= self.cfg.max_inflight_accums)
+                    or len(batch_gets) + len(new_units) > _capi.GEMM_MAX_GETS):
+                flush()
+                new_units = [u for u in units if u not in launched]
+            ga, gb = views[i]
+            sub = (m0, m1, n0, n1, k0, k1) != (0, len(op.m_bound), 0, len(op.n_bound), 0, len(op.k_bound))
+            if sub:
+                ga = _capi.UmView(ga.base, ga.row_lo + m0, ga.row_lo + m1, ga.col_lo + k0, ga.col_lo + k1, ga.pitch,
+                                  ga.dtype, ga.device)
+                gb = _capi.UmView(gb.base, gb.row_lo + k0, gb.row_lo + k1, gb.col_lo + n0, gb.col_lo + n1, gb.pitch,
+                                  gb.dtype, gb.device)
+            if remote and not self.cfg.fused_accumulate:
+                # unfused remote update (scratch GEMM + K3): its pulls must have landed
+                flush()
+                batch_gets.extend(new_units)
+                flush()
+                plan.actions.append(("scratch", op, ga, gb))
+                st.launches += 2
+                st.peak_ops_per_launch = max(st.peak_ops_per_launch, 1)
+                st.peak_inflight_accums = max(st.peak_inflight_accums, 1)
+                continue
+            for u in new_units:
+                gets_slot[u] = len(batch_gets)
+                batch_gets.append(u)
+            cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+            cl = op.c_local
+            gc = cseg.um_view(cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
+            g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
+            g.a_get = int(s.a_src[i] >= 0 and in_kernel[s.a_src[i]])
+            g.b_get = int(s.b_src[i] >= 0 and in_kernel[s.b_src[i]])
+            g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot)
+            if self.signals is not None and i in self.signals:
+                g.done_flag = self.signals[i][1](m0, m1)
+            batch.append(g)
+            batch_remote += int(remote)
+        flush()
+        # RunStats report the reference's execution order (runtime.py:213-236),
+        # whatever order the device runs the (sub-)ops in
+        st.executed_ops = list(s.ops)
+        st.a_requests = [op.a_tile for op in s.ops]
+        st.b_requests = [op.b_tile for op in s.ops]
+        plan.final_waits = [j for j in range(nf) if not in_kernel[j] and not waited[j]]
+        st.peak_inflight_gemms = 1 if s.ops else 0
+        return plan
+
+    def _replay(self, plan: "_IssuePlan"):
+        lib = _capi.load()
+        fab = self.fab
+        with torch.cuda.device(self.dev):
+            events = {}
+            gsp = ctypes.c_void_p(self.gs.cuda_stream)
+            for j, src, dst in plan.host_fetches:        # K2 on the copy engines, first-use order
+                _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get")
+                ev = torch.cuda.Event()
+                ev.record(self.gs)
+                events[j] = ev
+            csp = ctypes.c_void_p(self.cs.cuda_stream)
+            for act in plan.actions:
+                if act[0] == "launch":
+                    if TRACE_ENABLED:
+                        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        t0.record(self.cs)
+                    _capi.check(lib.um_gemm_launch(ctypes.c_void_p(act[1]), csp), "um_gemm_launch")
+                    if TRACE_ENABLED:
+                        t1.record(self.cs)
+                        TRACE.append((t0, t1, act[2]))
+                elif act[0] == "wait":
+                    self.cs.wait_event(events[act[1]])
+                else:
+                    self._scratch_gemm(*act[1:])
+            for j in plan.final_waits:
+                self.cs.wait_event(events[j])
+            # join the get stream back even when it carried nothing (keeps the
+            # multiply capturable into a CUDA graph: no unjoined forked stream)
+            ev = torch.cuda.Event()
+            ev.record(self.gs)
+            self.cs.wait_event(ev)
+            self.done = torch.cuda.Event()
+            self.done.record(self.cs)
+        fab.counters.merge(plan.traffic)
+        t = plan.stats
+        self.stats = RunStats(list(t.executed_ops), list(t.a_requests), list(t.b_requests), t.peak_inflight_gemms,
+                              t.peak_inflight_accums, t.pool_acquired, t.pool_released, t.pool_peak, 0, t.gets,
+                              t.staged_bytes, t.launches, t.peak_ops_per_launch)
+
+    def _operand_view(self, name, t, loc, src_idx, staged):
+        M = self._mat(name)
+        if src_idx < 0:
+            seg = M.segment(t, M.replica_of(self.caller))
+            return seg.um_view(loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi)
+        f = self.sched.fetches[src_idx]
+        buf = staged[src_idx]
+        return _capi.UmView(buf.data_ptr(), loc.rows.lo - f.r0, loc.rows.hi - f.r0, loc.cols.lo - f.c0,
+                            loc.cols.hi - f.c0, buf.stride(0), um_dtype(M.dtype), self.dev)
+
+    def _scratch_gemm(self, op, ga, gb):
+        """Unfused remote update: GEMM into zeroed scratch, then K3 accumulate."""
+        lib = _capi.load()
+        m, n = len(op.m_bound), len(op.n_bound)
+        pitch = pitch_for(n, torch.float32)
+        with torch.cuda.stream(self.cs):
+            scratch = torch.zeros((m, pitch), dtype=torch.float32, device=f"cuda:{self.dev}")
+        self.buffers.append(scratch)
+        gs = _capi.UmView(scratch.data_ptr(), 0, m, 0, n, pitch, _capi.UM_F32, self.dev)
+        _capi.check(lib.um_gemm_acc(ctypes.byref(ga), ctypes.byref(gb), ctypes.byref(gs),
+                                    ctypes.c_void_p(self.cs.cuda_stream)), "um_gemm_acc")
+        cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+        dst = cseg.um_view(op.c_local.rows.lo, op.c_local.rows.hi, op.c_local.cols.lo, op.c_local.cols.hi)
+        with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
+            _capi.check(lib.um_accumulate(ctypes.byref(gs), ctypes.byref(dst), ctypes.c_void_p(self.cs.cuda_stream)),
+                        "um_accumulate")

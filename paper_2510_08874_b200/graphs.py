@@ -22,6 +22,7 @@ import dataclasses
 
 import torch
 
+from paper_2510_08874_b200 import engine as eng
 from paper_2510_08874_b200 import runtime as rt
 from paper_2510_08874_b200.errors import ContractError
 
@@ -43,7 +44,7 @@ class CapturedMultiply:
         torch.cuda.synchronize()
         before = fab.counters.__class__(fab.counters.nprocs)
         before.merge(fab.counters)
-        trace, rt.TRACE_ENABLED = rt.TRACE_ENABLED, False
+        trace, eng.TRACE_ENABLED = eng.TRACE_ENABLED, False
         self.graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -51,7 +52,7 @@ class CapturedMultiply:
             with torch.cuda.graph(self.graph, stream=side):
                 self.stats = rt.execute_multiply(A, B, C, cfg)
         finally:
-            rt.TRACE_ENABLED = trace
+            eng.TRACE_ENABLED = trace
         # the capture ran the host-side counting of one multiply but executed
         # nothing: keep that as the per-replay delta and restore the counters
         self.delta = fab.counters.__class__(fab.counters.nprocs)

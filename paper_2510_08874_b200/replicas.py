@@ -1,0 +1,193 @@
+"""K4: replica reduction (distmatrix.py:211-232), barrier form and overlapped form."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from paper_2510_08874_b200 import _capi
+from paper_2510_08874_b200.config import ExecConfig
+from paper_2510_08874_b200.distmatrix import DistributedMatrix
+from paper_2510_08874_b200.engine import _current_events, _join_current
+from paper_2510_08874_b200.opgen import Stationarity
+from paper_2510_08874_b200.schedule import DirectSchedule, lower_direct
+
+
+def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None,
+                    rows: tuple[int, int] | None = None):
+    """replica[origin] += sum_{r != origin} replica[r] (in r order), K4 on device.
+
+    distributed: tile rows are split into c slices; slice j is reduced by the
+    GPU of replica j's tile owner (slice `origin` by the origin owner), which
+    pulls that slice from every other replica over NVLink and adds the sum
+    into the origin's slice.
+    """
+    fab = C.fabric
+    fab._require_data()
+    lib = _capi.load()
+    if start_events is None:
+        start_events = _current_events(fab)
+    done = []
+    for t in C.grid.tiles():
+        dst = C.segment(t, origin)
+        if dst.length == 0:
+            continue
+        srcs = [C.segment(t, r) for r in range(C.c) if r != origin]
+        nslices = C.c if distributed else 1
+        lo, hi = 0, dst.rows
+        if rows is not None:     # restrict to a global row window
+            tb = C.tile_bounds(t)
+            lo, hi = max(rows[0], tb.rows.lo) - tb.rows.lo, min(rows[1], tb.rows.hi) - tb.rows.lo
+            if hi <= lo:
+                continue
+        for j in range(nslices):
+            r0, r1 = lo + (hi - lo) * j // nslices, lo + (hi - lo) * (j + 1) // nslices
+            if r1 <= r0:
+                continue
+            reducer = C.owner_rank(t, j) if distributed else dst.owner
+            if not fab.is_local(reducer):
+                continue
+            dev = fab.device_of(reducer)
+            stream = fab.stream(reducer, "reduce")
+            for ev in start_events:
+                stream.wait_event(ev)
+            dv = dst.um_view(r0, r1, 0, dst.cols)
+            sv = (_capi.UmView * len(srcs))(*[s.um_view(r0, r1, 0, s.cols) for s in srcs])
+            with torch.cuda.device(dev):
+                _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), ctypes.c_void_p(stream.cuda_stream)),
+                            "um_reduce_replicas")
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done.append(ev)
+    _join_current(fab, done)
+    if fab.world.size > 1:
+        fab.synchronize()
+    return done
+
+
+class _ReduceOverlap:
+    """Replica reduction overlapped with the GEMMs (replicated C, Stationary C).
+
+    Every C tile is cut into c * panels row sub-slices (multiples of 256 rows,
+    the K1 tile height); sub-slice k is reduced by the owner of replica
+    k mod c (the distributed K4 of reduce_replicas, at finer grain, so every
+    reducer's work arrives spread over the GEMM).  Each rank's ops are split at
+    the sub-slice rows and carry a done_flag pointing at a word on the
+    sub-slice's reducer (symmetric heap: a peer or IPC-mapped address); the K1
+    epilogue adds the number of finished ops there (release, system scope).
+    The reducer's stream waits (um_wait_geq, a stream memory operation, no SM
+    held) for every contributing op of every replica in this run, then runs
+    K4 for the sub-slice.  Flags only grow: run e waits for e * expected.
+    """
+
+    def __init__(self, A, B, C, cfg: ExecConfig):
+        fab = C.fabric
+        p, c = fab.nprocs, C.c
+        self.C = C
+        self.subs = {}
+        n = c * cfg.reduce_panels
+        for t in C.grid.tiles():
+            rows = len(C.tile_bounds(t).rows)
+            cuts = sorted({0, rows} | {rows * s // n // 256 * 256 for s in range(1, n)})
+            self.subs[t] = [(cuts[k], cuts[k + 1], k % c) for k in range(len(cuts) - 1)]
+        counts = [0] * p
+        self.word = {}
+        for t, lst in self.subs.items():
+            for k, (_, _, rep) in enumerate(lst):
+                red = C.owner_rank(t, rep)
+                self.word[(t, k)] = (red, counts[red])
+                counts[red] += 1
+        # flag words live in the symmetric heap (same allocation order on every process)
+        self.flag_segs = [fab.alloc_tile(r, 1, max(1, counts[r]), torch.float32) for r in range(p)]
+        for seg in self.flag_segs:
+            if seg.storage is not None:
+                with torch.cuda.device(seg.device):
+                    seg.storage.zero_()
+        fab.heap.exchange()
+        # ops contributing to each sub-slice, over every replica's owner (host-only planning)
+        self.expected = {}
+        for r in range(p):
+            for op in lower_direct(A, B, C, cfg, r).ops:
+                lo, hi = op.c_local.rows.lo, op.c_local.rows.hi
+                for k, (r0, r1, _) in enumerate(self.subs[op.c_tile]):
+                    if lo < r1 and r0 < hi:
+                        self.expected[(op.c_tile, k)] = self.expected.get((op.c_tile, k), 0) + 1
+        self.epoch = 0
+        if fab.world.size > 1:
+            fab.synchronize()        # zeroed flags in place before any process can signal
+
+    def sub_slice_of(self, t, row: int) -> int:
+        """Index of the sub-slice of C tile t holding tile-local `row`."""
+        for k, (r0, r1, _) in enumerate(self.subs[t]):
+            if r0 <= row < r1:
+                return k
+        raise AssertionError("row outside its C tile")
+
+    def flag_ptr(self, t, k) -> int:
+        red, idx = self.word[(t, k)]
+        return self.flag_segs[red].ptr + 4 * idx
+
+    def signals_for(self, sched: DirectSchedule) -> dict:
+        sig = {}
+        for i, op in enumerate(sched.ops):
+            t, lo, hi = op.c_tile, op.c_local.rows.lo, op.c_local.rows.hi
+            cuts = [r0 - lo for r0, _, _ in self.subs[t] if lo < r0 < hi]
+
+            def flag(m0, m1, t=t, lo=lo):
+                return self.flag_ptr(t, self.sub_slice_of(t, lo + m0))
+
+            sig[i] = (cuts, flag)
+        return sig
+
+    def reduce(self, start_events) -> list:
+        """Enqueue wait + K4 per sub-slice on the reducers' streams; return done events."""
+        C, fab = self.C, self.C.fabric
+        lib = _capi.load()
+        self.epoch += 1
+        done = []
+        for t, lst in self.subs.items():
+            dst = C.segment(t, 0)
+            if dst.length == 0:
+                continue
+            srcs = [C.segment(t, r) for r in range(1, C.c)]
+            for k, (r0, r1, rep) in enumerate(lst):
+                red = C.owner_rank(t, rep)
+                if not fab.is_local(red) or r1 <= r0:
+                    continue
+                dev = fab.device_of(red)
+                stream = fab.stream(red, "reduce")
+                for ev in start_events:
+                    stream.wait_event(ev)
+                sp = ctypes.c_void_p(stream.cuda_stream)
+                exp = self.expected.get((t, k), 0)
+                with torch.cuda.device(dev):
+                    if exp:
+                        _capi.check(lib.um_wait_geq(ctypes.c_void_p(self.flag_ptr(t, k)),
+                                                    (self.epoch * exp) & 0xFFFFFFFF, sp), "um_wait_geq")
+                    dv = dst.um_view(r0, r1, 0, dst.cols)
+                    sv = (_capi.UmView * len(srcs))(*[s_.um_view(r0, r1, 0, s_.cols) for s_ in srcs])
+                    _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), sp), "um_reduce_replicas")
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                done.append(ev)
+        return done
+
+
+def _overlap_for(A, B, C, cfg: ExecConfig):
+    if not (cfg.overlap_reduce and cfg.reduce_distributed and C.c > 1
+            and cfg.stationarity is Stationarity.STATIONARY_C):
+        return None
+    # processes time-sharing one GPU (no MPS) could park a stream wait that only
+    # another process's kernel can satisfy: keep the barrier + K4 path there
+    if C.fabric.devices_shared_across_processes() and os.environ.get("UM_OVERLAP_SHARED") != "1":
+        return None
+    key = ("ovl", id(A), id(B), cfg.reduce_panels, cfg.staging, cfg.same_device_gets)
+    cache = C.__dict__.setdefault("_ovl_cache", {})
+    hit = cache.get(key)
+    if hit is not None and hit[0] is A and hit[1] is B:
+        return hit[2]
+    ovl = _ReduceOverlap(A, B, C, cfg)
+    cache[key] = (A, B, ovl)
+    return ovl

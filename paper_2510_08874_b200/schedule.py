@@ -1,0 +1,239 @@
+"""Schedule lowering of one rank's direct execution (host only, no device work).
+
+The caller's op list from the C++ planner, rotated by the reference's
+iteration offset (runtime.py:89-93,213-214); remote operand slices
+deduplicated into fetch-once pulls (the reference re-fetches whole tiles per
+op: distmatrix.py:158, runtime.py:219-231); and `plan_bands`, which splits
+ops into sub-ops and pulls into bands so each (sub-)op waits on the device
+only for the data it reads.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from paper_2510_08874_b200 import _capi, opgen
+from paper_2510_08874_b200.config import ExecConfig
+from paper_2510_08874_b200.tiling import TileIdx
+
+
+def iteration_offset(stationary_tile: TileIdx, nops: int) -> int:
+    """(i + j) mod nops of the first op's stationary tile (runtime.py:89-93)."""
+    out = ctypes.c_int64(0)
+    _capi.check(_capi.load().um_iteration_offset(stationary_tile.i, stationary_tile.j, nops, ctypes.byref(out)),
+                "iteration_offset")
+    return int(out.value)
+
+
+@dataclass
+class _Fetch:
+    mat: str                 # "A" | "B"
+    tile: TileIdx
+    replica: int
+    owner: int
+    r0: int                  # tile-local bounding box of the needed slices
+    r1: int
+    c0: int
+    c1: int
+    first_use: int
+
+
+@dataclass
+class DirectSchedule:
+    """Lowered direct-execution schedule of one rank."""
+
+    caller: int
+    ops: list                        # rotated op list
+    fetches: list                    # _Fetch in first-use order
+    a_src: list                      # per op: fetch index or -1 (read in place)
+    b_src: list
+    c_remote: list                   # per op: True if the C tile belongs to another rank
+
+
+def _in_place(fabric, owner: int, caller: int, cfg: ExecConfig) -> bool:
+    if owner == caller:
+        return True
+    if cfg.same_device_gets == "direct" and fabric.world.size == 1 and not fabric.placement_only:
+        return fabric.device_of(owner) == fabric.device_of(caller)
+    return False
+
+
+def rotated_ops(A, B, C, cfg: ExecConfig, caller: int) -> list:
+    """The caller's op list in execution order (runtime.py:207,213-214)."""
+    ops = opgen.generate(cfg.stationarity, A, B, C, caller)
+    if ops:
+        s = iteration_offset(ops[0].stationary_tile(cfg.stationarity), len(ops))
+        ops = ops[s:] + ops[:s]
+    return ops
+
+
+def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None) -> DirectSchedule:
+    """Rotated op list + fetch-once staging plan (host-side, no device work).
+
+    `ops` overrides the planner's list (e.g. ops restricted to a row panel).
+    Schedules of the planner's own list are cached per (matrices, knobs, rank):
+    placement is immutable, so repeated multiplies skip the host work."""
+    if ops is None:
+        key = (id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets, caller)
+        cache = A.__dict__.setdefault("_sched_cache", {})
+        hit = cache.get(key)
+        if hit is not None and hit[0] is B and hit[1] is C:
+            return hit[2]
+        sched = lower_direct(A, B, C, cfg, caller, rotated_ops(A, B, C, cfg, caller))
+        cache[key] = (B, C, sched)
+        return sched
+    fabric = A.fabric
+    fetches: list[_Fetch] = []
+    index: dict = {}
+    a_src, b_src, c_remote = [], [], []
+    for i, op in enumerate(ops):
+        for name, M, t, loc, srcs in (("A", A, op.a_tile, op.a_local, a_src), ("B", B, op.b_tile, op.b_local, b_src)):
+            rep = M.replica_of(caller)
+            owner = M.owner_rank(t, rep)
+            if _in_place(fabric, owner, caller, cfg):
+                srcs.append(-1)
+                continue
+            key = (name, t)
+            j = index.get(key)
+            if cfg.staging == "tile":
+                b = M.tile_bounds(t)
+                r0, r1, c0, c1 = 0, len(b.rows), 0, len(b.cols)
+            else:
+                r0, r1, c0, c1 = loc.rows.lo, loc.rows.hi, loc.cols.lo, loc.cols.hi
+            if j is None:
+                index[key] = len(fetches)
+                srcs.append(len(fetches))
+                fetches.append(_Fetch(name, t, rep, owner, r0, r1, c0, c1, i))
+            else:
+                f = fetches[j]
+                f.r0, f.r1, f.c0, f.c1 = min(f.r0, r0), max(f.r1, r1), min(f.c0, c0), max(f.c1, c1)
+                srcs.append(j)
+        c_owner = C.owner_rank(op.c_tile, C.replica_of(caller))
+        c_remote.append(c_owner != caller)
+    return DirectSchedule(caller, ops, fetches, a_src, b_src, c_remote)
+
+
+_SPLIT_BYTES = 64 << 20       # an op whose first use pulls at least this much runs as sub-ops
+_SPLIT_MIN = 2048             # minimum extent of a sub-op along the split dimension
+
+
+def _tma_ok(v) -> bool:
+    """K1 reads a view in place iff its column start, pitch and base are 16-byte aligned."""
+    es = 2 if v.dtype == _capi.UM_BF16 else 4
+    return (v.col_lo * es) % 16 == 0 and (v.pitch * es) % 16 == 0 and (v.base or 0) % 16 == 0
+
+
+def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: dict | None = None):
+    """Host-only planning of a rank's in-kernel pulls (no device work).
+
+    Returns (items, bands, need):
+      items  (op, sub, m0, m1, n0, n1, k0, k1): the ops in execution order, an
+             op that must first pull >= _SPLIT_BYTES split into sub-ops
+             (offsets relative to the op's m / n / k ranges);
+      bands  per fetch: (r0, r1, c0, c1) rectangles of the staged slice, cut
+             along the dimension in which the (sub-)ops' slices differ, bands
+             no op reads dropped (None for copy-engine fetches);
+      need   (item, fetch) -> indices of the bands the item reads.
+    row_cuts   op -> cut positions along its m range (relative): the op is split
+             exactly there and nowhere else (overlapped replica reduction:
+             every item then lies in one reduction sub-slice of its C tile).
+    """
+    nf = len(s.fetches)
+    # Sub-ops: an op that must first pull a large amount (cfg4: whole 8192^2
+    # A and B tiles) runs as sub-ops that each wait only for their part of
+    # the pull.  Default split: along m when the pulled A dominates, along n
+    # when B does (rows / columns of C: no extra C traffic, the tensor cores
+    # start once B / A and the first A / B band have landed).  k_split > 1
+    # instead cuts k into slabs (every sub-op waits for one A and one B
+    # slab, at the price of one more fp32 C read-modify-write per slab).
+    first_user: dict = {}
+    for i in range(len(s.ops)):
+        for j in (s.a_src[i], s.b_src[i]):
+            if j >= 0:
+                first_user.setdefault(j, i)
+
+    def pulled(i, j):
+        if j < 0 or not in_kernel[j] or first_user[j] != i:
+            return 0
+        f = s.fetches[j]
+        return (f.r1 - f.r0) * (f.c1 - f.c0) * 2
+
+    items = []                       # (op, sub, dm0, dm1, dn0, dn1, k0, k1), offsets relative to the op
+    for i, op in enumerate(s.ops):
+        mlen, nlen, klen = len(op.m_bound), len(op.n_bound), len(op.k_bound)
+        pa = pulled(i, s.a_src[i])
+        pb = pulled(i, s.b_src[i]) if s.b_src[i] != s.a_src[i] else 0
+        unfused_remote = s.c_remote[i] and not cfg.fused_accumulate
+        nsub, dim = 1, None
+        if row_cuts is not None and i in row_cuts:
+            cuts_i = sorted({0, mlen} | {c for c in row_cuts[i] if 0 < c < mlen})
+            for t in range(len(cuts_i) - 1):
+                items.append((i, t, cuts_i[t], cuts_i[t + 1], 0, nlen, 0, klen))
+            continue
+        if not unfused_remote and pa + pb >= _SPLIT_BYTES:
+            if cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
+            elif cfg.mn_split > 1 and pa >= pb and mlen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.mn_split, mlen // _SPLIT_MIN)), "m"
+            elif cfg.mn_split > 1 and pb > pa and nlen >= 2 * _SPLIT_MIN:
+                nsub, dim = int(min(cfg.mn_split, nlen // _SPLIT_MIN)), "n"
+        full = {"m": mlen, "n": nlen, "k": klen}
+        cut = sorted({0, full[dim]} | {full[dim] * t // nsub // 64 * 64 for t in range(1, nsub)}) if dim else [0, 0]
+        for t in range(len(cut) - 1):
+            lo, hi = cut[t], cut[t + 1]
+            mm = (lo, hi) if dim == "m" else (0, mlen)
+            nn = (lo, hi) if dim == "n" else (0, nlen)
+            kk = (lo, hi) if dim == "k" else (0, klen)
+            items.append((i, t, *mm, *nn, *kk))
+
+    # device order: items writing the same C region run back to back (K1 chains
+    # them into one accumulator: one epilogue per tile), groups in order of first
+    # appearance; the pulls then arrive in the order those chains need them.
+    # (RunStats keep the reference's execution order: this is device-internal.)
+    if cfg.chain_order:
+        def ckey(it):
+            i, t, m0, m1, n0, n1, k0, k1 = it
+            cl = s.ops[i].c_local
+            return (s.ops[i].c_tile, cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
+
+        first = {}
+        for pos, it in enumerate(items):
+            first.setdefault(ckey(it), pos)
+        items = sorted(items, key=lambda it: first[ckey(it)])      # stable: k order kept inside a chain
+
+    # in-kernel pulls are cut into bands along the dimension in which the
+    # (sub-)ops' slices differ, so an op waits only for the slab it reads
+    # (cfg5: a 64 MiB B tile feeds 4 ops with one 16 MiB k-slab each)
+    uses = [[] for _ in range(nf)]
+    for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
+        op = s.ops[i]
+        a, b = op.a_local, op.b_local
+        for src, (r0, r1, c0, c1) in ((s.a_src[i], (a.rows.lo + m0, a.rows.lo + m1, a.cols.lo + k0, a.cols.lo + k1)),
+                                      (s.b_src[i], (b.rows.lo + k0, b.rows.lo + k1, b.cols.lo + n0, b.cols.lo + n1))):
+            if src >= 0:
+                f = s.fetches[src]
+                uses[src].append((it, r0 - f.r0, r1 - f.r0, c0 - f.c0, c1 - f.c0))
+    bands = [None] * nf              # per fetch: list of (r0, r1, c0, c1) in staged-buffer coordinates
+    need = {}                        # (item, fetch) -> band indices
+    for j, f in enumerate(s.fetches):
+        if not in_kernel[j]:
+            continue
+        H, W = f.r1 - f.r0, f.c1 - f.c0
+        sl = uses[j]
+        # cells of the grid spanned by the slices' row and column boundaries;
+        # keep the cells some slice reads
+        rcuts = sorted({x for _, r0, r1, _, _ in sl for x in (r0, r1)})
+        ccuts = sorted({x for _, _, _, c0, c1 in sl for x in (c0, c1)})
+        cand = [(r0, r1, c0, c1) for r0, r1 in zip(rcuts, rcuts[1:]) for c0, c1 in zip(ccuts, ccuts[1:])]
+
+        def key(bd, u):
+            return bd[0] < u[2] and u[1] < bd[1] and bd[2] < u[4] and u[3] < bd[3]
+
+        cand = [bd for bd in cand if any(key(bd, u) for u in sl)]    # drop cells no op reads
+        if len(cand) > 16:
+            cand = [(0, H, 0, W)]
+        bands[j] = cand
+        for u in sl:
+            need[(u[0], j)] = [k for k, bd in enumerate(cand) if key(bd, u)]
+    return items, bands, need

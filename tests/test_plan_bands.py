@@ -12,6 +12,7 @@ import pytest
 
 from paper_2510_08874_b200 import ExecConfig, Stationarity
 from paper_2510_08874_b200 import runtime as rt
+from paper_2510_08874_b200 import schedule as sch
 from paper_2510_08874_b200.cli import build_problem
 from paper_2510_08874_b200.fabric import Fabric, LinkTable
 
@@ -94,8 +95,8 @@ def test_cfg4_p8_whole_tile_op_split_along_m():
 
 @pytest.mark.parametrize("seed", range(16))
 def test_random_configs_bands_cover_slices(seed, monkeypatch):
-    monkeypatch.setattr(rt, "_SPLIT_BYTES", 1 << 10)
-    monkeypatch.setattr(rt, "_SPLIT_MIN", 16)
+    monkeypatch.setattr(sch, "_SPLIT_BYTES", 1 << 10)
+    monkeypatch.setattr(sch, "_SPLIT_MIN", 16)
     rnd = random.Random(seed)
     p = rnd.choice([2, 4, 6, 8, 12])
     m, n, k = (rnd.randint(8, 300) for _ in range(3))

@@ -25,6 +25,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2510_08874_b200 import ExecConfig, Stationarity, execute_multiply  # noqa: E402
+from paper_2510_08874_b200 import engine as eng  # noqa: E402
 from paper_2510_08874_b200 import runtime as rt  # noqa: E402
 from paper_2510_08874_b200.cli import build_problem  # noqa: E402
 
@@ -45,17 +46,17 @@ def run_one(name, p, steps, warmup, stationarity, extra):
 
         cap = CapturedMultiply(A, B, C, cfg)
         torch.cuda.synchronize()
-    rt.TRACE.clear()
-    rt.TRACE_ENABLED = cap is None
+    eng.TRACE.clear()
+    eng.TRACE_ENABLED = cap is None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(steps):
         stats = cap.replay() if cap is not None else execute_multiply(A, B, C, cfg)
     e1.record()
     torch.cuda.synchronize()
-    rt.TRACE_ENABLED = False
+    eng.TRACE_ENABLED = False
     ms = e0.elapsed_time(e1) / steps
-    kms = sum(s.elapsed_time(e) for s, e, _ in rt.TRACE) / steps if rt.TRACE else 0.0
+    kms = sum(s.elapsed_time(e) for s, e, _ in eng.TRACE) / steps if eng.TRACE else 0.0
     solo = {}
     if p > 1 and os.environ.get("UM_MATRIX_SOLO", "1") == "1":
         # each rank ALONE on the GPU (its pulls read HBM instead of NVLink): the
