@@ -71,7 +71,7 @@ class ExecConfig:
     mn_split: int = 4
     overlap_reduce: bool = True
     chain_order: bool = True
-    reduce_panels: int = 2
+    reduce_panels: int = 4
     k_split: int = 0
 
     def __post_init__(self):

@@ -184,7 +184,8 @@ struct alignas(64) LaunchArgs {
   int nwork, total_tiles;
   int* counters;              // per-stream {tile, done clusters, get chunk, get done[MAX_GETS]}
   int ngets, total_chunks;
-  int nslots, pad_;
+  int nslots;
+  uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
   SignalSlot slots[MAX_SLOTS];
   CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
   Work inl_works[MAX_INLINE_OPS];
@@ -597,12 +598,19 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
     // helps and the first ops' operands land first.  No wait on anything but its
     // own loads: deadlock-free whatever the SMs are doing.
     int* const chunk_ctr = &args.counters[2];
+    const uint64_t t_begin = ptx::globaltimer();
     int* const done = &args.counters[3];
     for (;;) {
       int c = 0;
       if (lane == 0) c = atomicAdd(chunk_ctr, 1);
       c = __shfl_sync(0xffffffffu, c, 0);
       if (c >= args.total_chunks) break;
+      if (args.get_ns_per_chunk) {
+        // profiling knob (UM_GET_GBPS): release chunk c no earlier than c chunk-times
+        // after the launch, i.e. emulate a link of that bandwidth on one GPU
+        const uint64_t due = t_begin + (uint64_t)c * args.get_ns_per_chunk;
+        while (ptx::globaltimer() < due) __nanosleep(200);
+      }
       int j = 0;
       while (j + 1 < args.ngets && args.gets[j + 1].chunk_start <= c) ++j;
       const GetDesc& g = args.gets[j];
@@ -1110,6 +1118,13 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   }
   args.ngets = ngets;
   args.total_chunks = chunks;
+  // UM_GET_GBPS=<GB/s>: pace the in-kernel pulls to that rate (profiling: a
+  // one-GPU run with pulls at NVLink speed)
+  static const double get_gbps = [] {
+    const char* e = getenv("UM_GET_GBPS");
+    return (e && *e) ? atof(e) : 0.0;
+  }();
+  args.get_ns_per_chunk = get_gbps > 0 ? (uint32_t)(GET_CHUNK_BYTES / get_gbps + 0.5) : 0u;
   P->ngets = ngets;
   P->nslots = args.nslots;
   // gets only / signals only: still one launch (get warps; slots with no tile

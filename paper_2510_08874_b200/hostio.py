@@ -107,14 +107,11 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
             if not ops:
                 continue
             # panel schedules (and their issue plans) are cached like full ones
-            pkey = ("panel", id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets, r, r0, r1)
-            cache = A.__dict__.setdefault("_sched_cache", {})
-            hit = cache.get(pkey)
-            if hit is not None and hit[0] is B and hit[1] is C:
-                sched = hit[2]
-            else:
-                sched = rt.lower_direct(A, B, C, cfg, r, ops=ops)
-                cache[pkey] = (B, C, sched)
+            pkey = ("panel", cfg.stationarity, cfg.staging, cfg.same_device_gets, r, r0, r1)
+            cache = rt.schedule_cache(A, B, C)
+            sched = cache.get(pkey)
+            if sched is None:
+                sched = cache[pkey] = rt.lower_direct(A, B, C, cfg, r, ops=ops)
             rt._count_reference_traffic(A, B, C, cfg, sched)
             runs.append(rt._RankRun(A, B, C, cfg, sched, ready).issue())
         done = [run.done for run in runs]

@@ -43,7 +43,8 @@ from paper_2510_08874_b200.fabric import ELEM_BYTES, AccumulateMode, pitch_for, 
 from paper_2510_08874_b200.opgen import LocalMatMulOp, Stationarity  # noqa: F401
 from paper_2510_08874_b200.replicas import _overlap_for, _ReduceOverlap, reduce_replicas  # noqa: F401
 from paper_2510_08874_b200.schedule import (  # noqa: F401
-    DirectSchedule, _Fetch, _in_place, _tma_ok, iteration_offset, lower_direct, plan_bands, rotated_ops)
+    DirectSchedule, _Fetch, _in_place, _tma_ok, iteration_offset, lower_direct, plan_bands, rotated_ops,
+    schedule_cache)
 from paper_2510_08874_b200.tiling import TileIdx  # noqa: F401
 
 __all__ = ["ExecConfig", "BufferPool", "RunStats", "iteration_offset", "local_gemm", "run_direct",
@@ -254,8 +255,8 @@ def _cross_process(A, B, C, cfg: ExecConfig) -> bool:
     fab = A.fabric
     if fab.world.size == 1:
         return False
-    key = ("cross", id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets)
-    cache = A.__dict__.setdefault("_sched_cache", {})
+    key = ("cross", cfg.stationarity, cfg.staging, cfg.same_device_gets)
+    cache = schedule_cache(A, B, C)
     if key in cache:
         return cache[key]
     proc = fab.process_of

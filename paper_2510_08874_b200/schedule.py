@@ -68,6 +68,24 @@ def rotated_ops(A, B, C, cfg: ExecConfig, caller: int) -> list:
     return ops
 
 
+_MAX_CACHED_PAIRS = 8      # distinct (B, C) partners whose schedules (and staging pools) A keeps
+
+
+def schedule_cache(A, B, C) -> dict:
+    """A's cache of schedules/plans for the partner pair (B, C).  Entries hold
+    staging pools on the device, so only the most recently used
+    _MAX_CACHED_PAIRS pairs are kept (least recently used dropped)."""
+    pairs = A.__dict__.setdefault("_sched_pairs", {})
+    key = (id(B), id(C))
+    hit = pairs.pop(key, None)
+    if hit is None or hit[0] is not B or hit[1] is not C:
+        hit = (B, C, {})
+    pairs[key] = hit                      # most recent last
+    while len(pairs) > _MAX_CACHED_PAIRS:
+        pairs.pop(next(iter(pairs)))
+    return hit[2]
+
+
 def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None) -> DirectSchedule:
     """Rotated op list + fetch-once staging plan (host-side, no device work).
 
@@ -75,14 +93,12 @@ def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None)
     Schedules of the planner's own list are cached per (matrices, knobs, rank):
     placement is immutable, so repeated multiplies skip the host work."""
     if ops is None:
-        key = (id(B), id(C), cfg.stationarity, cfg.staging, cfg.same_device_gets, caller)
-        cache = A.__dict__.setdefault("_sched_cache", {})
+        key = ("sched", cfg.stationarity, cfg.staging, cfg.same_device_gets, caller)
+        cache = schedule_cache(A, B, C)
         hit = cache.get(key)
-        if hit is not None and hit[0] is B and hit[1] is C:
-            return hit[2]
-        sched = lower_direct(A, B, C, cfg, caller, rotated_ops(A, B, C, cfg, caller))
-        cache[key] = (B, C, sched)
-        return sched
+        if hit is None:
+            hit = cache[key] = lower_direct(A, B, C, cfg, caller, rotated_ops(A, B, C, cfg, caller))
+        return hit
     fabric = A.fabric
     fetches: list[_Fetch] = []
     index: dict = {}
