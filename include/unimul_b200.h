@@ -133,8 +133,11 @@ typedef struct {
   int32_t c_remote;
   uint32_t wait_value;
   const uint32_t* wait_flag;
-  int32_t a_get, b_get;    /* um_gemm_acc_fused: 1 if this op's a / b operand is written by an
-                              in-kernel get of the same launch (must then be TMA-aligned) */
+  int32_t a_get, b_get;    /* um_gemm_acc_fused: 1-based index of the get whose band holds
+                              this op's a / b operand, waited for chunk by chunk (a: the
+                              rows of each tile, all k; b: the rows of each k-block) —
+                              the view must lie inside the band's columns and be
+                              TMA-aligned; 0 = resident or covered by get_mask          */
   uint64_t get_mask;       /* bit i: the op starts loading only after gets[i] has landed  */
   uint32_t* done_flag;     /* non-NULL: when every op of the launch sharing this flag has
                               written all of its C tiles, the kernel adds the number of

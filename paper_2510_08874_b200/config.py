@@ -44,6 +44,10 @@ class ExecConfig:
                          (um_wait_geq) while the GEMMs go on — no run-level
                          barrier between the GEMMs and the reduction.
       reduce_panels      sub-slices per replica and tile (>= 1).
+      fine_waits         an operand pulled into one band waits chunk by chunk
+                         (A: its tile's rows; B: each k-block's rows) instead of
+                         for the whole band, so the first tiles start as soon
+                         as their first rows land.
       chain_order        issue ops that write the same C region back to back
                          (K1 accumulates such a k-chain in TMEM and reduces
                          into C once per tile).
@@ -71,6 +75,7 @@ class ExecConfig:
     mn_split: int = 4
     overlap_reduce: bool = True
     chain_order: bool = True
+    fine_waits: bool = True
     reduce_panels: int = 4
     k_split: int = 0
 

@@ -108,6 +108,7 @@ struct alignas(16) Work {
   uint32_t wait_value;
   int32_t slot;               // completion-signal slot (-1: none)
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
+  int32_t a_fine, b_fine;     // 1-based get whose chunks A (per tile rows) / B (per k-block rows) wait for
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -120,6 +121,7 @@ struct alignas(16) GetDesc {
   int32_t rows, row_bytes;
   int32_t rows_per_chunk, nchunks;
   int32_t chunk_start, vec;       // vec: 16-byte aligned rows (vector path)
+  int32_t row0, pad_;             // first row of the band in its staging buffer (fine-grained waits)
 };
 
 __device__ __forceinline__ int find_work(const Work* works, int nwork, int t) {
@@ -168,6 +170,8 @@ constexpr int MAX_INLINE_OPS = UM_GEMM_MAX_INLINE_OPS;
 constexpr int MAX_GETS = UM_GEMM_MAX_GETS;
 constexpr int GET_CHUNK_BYTES = 32 * 1024;
 constexpr int MAX_SLOTS = UM_GEMM_MAX_SIGNALS;
+constexpr int MAX_CHUNK_FLAGS = 1 << 16;  // per-chunk landed flags (fine-grained waits)
+constexpr int CHUNK_FLAGS_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
 
 // Completion signal: once every tile of every op naming this slot has been
 // written (all epilogue warps of both CTAs of each tile arrive), the kernel
@@ -266,6 +270,41 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
       int stage = 0;
       uint32_t phase = 0;
       uint64_t landed = 0;   // in-kernel gets whose every chunk this producer has observed
+      // fine-grained waits: rows [r0, r1) of get g's band.  Fast path: the
+      // band's chunk count says it has fully landed (then never checked
+      // again); otherwise the flags of the chunks holding those rows, loaded
+      // 8 at a time so their latencies overlap.
+      auto wait_rows = [&](int g, int r0, int r1) {
+        if ((landed >> g) & 1ull) return;
+        const GetDesc& gd = args.gets[g];
+        if (ptx::ld_relaxed_gpu_s32(&args.counters[3 + g]) >= gd.nchunks) {
+          landed |= 1ull << g;
+        } else {
+          const int lo = max(r0 - gd.row0, 0), hi = min(r1 - gd.row0, gd.rows);
+          if (hi <= lo) return;
+          const int c_lo = gd.chunk_start + lo / gd.rows_per_chunk;
+          const int c_hi = gd.chunk_start + (hi - 1) / gd.rows_per_chunk;
+          const uint64_t t0 = ptx::globaltimer();
+          uint32_t spins = 0;
+          for (int c = c_lo; c <= c_hi; c += 8) {
+            const int n = min(8, c_hi - c + 1);
+            for (;;) {
+              int ok = 1;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < n) ok &= ptx::ld_relaxed_gpu_s32(&args.counters[CHUNK_FLAGS_OFF + c + i]) != 0;
+              if (ok) break;
+              __nanosleep(64);
+              if ((++spins & 0x3FFFu) == 0 && ptx::globaltimer() - t0 > 20000000000ull) {
+                printf("unimul_b200: chunk watchdog fired (block %d, get %d, chunk %d)\n", blockIdx.x, g, c);
+                __trap();
+              }
+            }
+          }
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        ptx::fence_proxy_async_global();
+      };
       int flag_ok = -1;      // highest work index whose external arrival flag has been observed
       for (int i = 0;; ++i) {
         int t;
@@ -322,6 +361,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
         const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
+        if (wk.a_fine) wait_rows(wk.a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
         // default: measured slower, 1437 -> 1143..1292 TFLOP/s on cfg2)
         auto prefetch = [&](int kb) {
@@ -342,6 +382,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           uint8_t* sb = smem_b + stage * C::B_BYTES;
           const int kcol = wk.a_col0 + kb * BK;
           const int krow = wk.b_row0 + kb * BK;
+          if (wk.b_fine) wait_rows(wk.b_fine - 1, krow, krow + BK);   // this k-block's B rows
           if constexpr (CG == 1) {
             ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pa);
           } else {
@@ -664,6 +705,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
       if (lane == 0) {
         __threadfence();
         atomicAdd(&done[j], 1);
+        if (c < MAX_CHUNK_FLAGS) ptx::st_release_gpu_s32(&args.counters[CHUNK_FLAGS_OFF + c], 1);
       }
     }
   }
@@ -771,7 +813,7 @@ static int* stream_counters(int device, cudaStream_t stream) {
   for (auto& e : table)
     if (e.first.first == device && e.first.second == stream) return e.second;
   int* p = nullptr;
-  constexpr size_t bytes = (3 + MAX_GETS + MAX_SLOTS) * sizeof(int);
+  constexpr size_t bytes = (CHUNK_FLAGS_OFF + MAX_CHUNK_FLAGS) * sizeof(int);
   if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
   // zero in stream order: torch's streams are non-blocking, so a plain
   // cudaMemset (legacy default stream) would race the first launch
@@ -899,6 +941,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     if (!inner_aligned(op.c)) op.c_remote = 1;
     if (ngets < 64 && (op.get_mask >> ngets) != 0)
       return fail(UM_EVALUE, "op waits on an in-kernel get outside the launch's list");
+    if (op.a_get < 0 || op.a_get > ngets || op.b_get < 0 || op.b_get > ngets)
+      return fail(UM_EVALUE, "a_get / b_get name a get outside the launch's list");
     if ((op.a_get && !inner_aligned(op.a)) || (op.b_get && !inner_aligned(op.b)))
       return fail(UM_ECONTRACT, "an operand delivered by an in-kernel get must be TMA-aligned (16-byte column start)");
   }
@@ -1013,6 +1057,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.wait_flag = op.wait_flag;
     w.wait_value = op.wait_value;
     w.wait_mask = op.get_mask;
+    w.a_fine = op.a_get;
+    w.b_fine = op.b_get;
     w.group = kn.group;
     // L2 eviction hints default to normal: measured on the box, evict_last on
     // the group-reused operand + evict_first on the streamed one lowered the
@@ -1112,12 +1158,19 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     g.rows_per_chunk = std::max(1, GET_CHUNK_BYTES / std::max(1, g.row_bytes));
     g.nchunks = g.rows && g.row_bytes ? (g.rows + g.rows_per_chunk - 1) / g.rows_per_chunk : 0;
     g.chunk_start = chunks;
+    g.row0 = (int32_t)gd.dst.row_lo;
     g.vec = ((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) | (uintptr_t)g.src_pitch |
               (uintptr_t)g.dst_pitch | (uintptr_t)g.row_bytes) & 15) == 0;
     chunks += g.nchunks;
   }
   args.ngets = ngets;
   args.total_chunks = chunks;
+  if (chunks > MAX_CHUNK_FLAGS)   // too many chunks for per-chunk flags: whole-band waits instead
+    for (Work& w : works) {
+      if (w.a_fine) w.wait_mask |= 1ull << (w.a_fine - 1);
+      if (w.b_fine) w.wait_mask |= 1ull << (w.b_fine - 1);
+      w.a_fine = w.b_fine = 0;
+    }
   // UM_GET_GBPS=<GB/s>: pace the in-kernel pulls to that rate (profiling: a
   // one-GPU run with pulls at NVLink speed)
   static const double get_gbps = [] {
@@ -1164,7 +1217,11 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   LaunchArgs& args = P->args;
   args.counters = stream_counters(P->device, stream);
   if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
-  if (P->ngets) UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + P->ngets) * sizeof(int), stream));
+  if (P->ngets) {
+    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + P->ngets) * sizeof(int), stream));
+    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + CHUNK_FLAGS_OFF, 0,
+                                  std::min(args.total_chunks, MAX_CHUNK_FLAGS) * sizeof(int), stream));
+  }
   if (P->nslots)
     UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 3 + MAX_GETS, 0, P->nslots * sizeof(int), stream));
   if (P->CG == 1) return launch<1, 256, 4>(args, P->device, stream);

@@ -90,6 +90,7 @@ class _RankRun:
     def issue(self):
         """Replay this rank's issue plan (built once per schedule and knob set)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
+               self.cfg.fine_waits,
                self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key)
         plans = self.sched.__dict__.setdefault("plans", {})
         plan = plans.get(key)
@@ -227,9 +228,19 @@ class _RankRun:
             cl = op.c_local
             gc = cseg.um_view(cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
             g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
-            g.a_get = int(s.a_src[i] >= 0 and in_kernel[s.a_src[i]])
-            g.b_get = int(s.b_src[i] >= 0 and in_kernel[s.b_src[i]])
-            g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot)
+            # an operand read from ONE band of this launch (inside its columns)
+            # waits chunk by chunk: A for its tile rows, B for each k-block's rows
+            fine = {}
+            for name, j, v in (("a", s.a_src[i], ga), ("b", s.b_src[i], gb)):
+                if self.cfg.fine_waits and j >= 0 and in_kernel[j] and len(need[(it, j)]) == 1:
+                    u = (j, need[(it, j)][0])
+                    br0, br1, bc0, bc1 = bands[j][u[1]]
+                    if (u in gets_slot and bc0 <= v.col_lo and v.col_hi <= bc1 and br0 <= v.row_lo
+                            and v.row_hi <= br1):
+                        fine[name] = u
+            g.a_get = gets_slot[fine["a"]] + 1 if "a" in fine else 0
+            g.b_get = gets_slot[fine["b"]] + 1 if "b" in fine else 0
+            g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot and u not in fine.values())
             if self.signals is not None and i in self.signals:
                 g.done_flag = self.signals[i][1](m0, m1)
             batch.append(g)

@@ -62,17 +62,22 @@ def run_one(name, p, steps, warmup, stationarity, extra):
         # each rank ALONE on the GPU (its pulls read HBM instead of NVLink): the
         # per-rank step time of a p-GPU run is max over ranks of this + the reduction
         from paper_2510_08874_b200 import run_direct
-        per = []
+        per, per_k1 = [], []
         for r in range(p):
             run_direct(A, B, C, cfg, r)
             torch.cuda.synchronize()
+            eng.TRACE.clear()
+            eng.TRACE_ENABLED = True
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record()
             for _ in range(steps):
                 run_direct(A, B, C, cfg, r)
             t1.record()
             torch.cuda.synchronize()
+            eng.TRACE_ENABLED = False
             per.append(t0.elapsed_time(t1) / steps)
+            # device time of the rank's K1 launch(es) alone (no host issue gap)
+            per_k1.append(sum(a.elapsed_time(b) for a, b, _ in eng.TRACE) / steps)
         red = 0.0
         if C.c > 1:
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -82,8 +87,33 @@ def run_one(name, p, steps, warmup, stationarity, extra):
             t1.record()
             torch.cuda.synchronize()
             red = t0.elapsed_time(t1) / steps
-        solo = {"rank_ms": per, "rank_ms_max": max(per), "reduce_ms_all_slices": red,
+        solo = {"rank_ms": per, "rank_ms_max": max(per), "rank_k1_ms": per_k1, "rank_k1_ms_max": max(per_k1),
+                "reduce_ms_all_slices": red,
                 "per_gpu_tflops_ranks": [flops / p / (t * 1e-3) / 1e12 for t in per]}
+        if C.c > 1:
+            # K4 over NVLink (model): bytes each reducer pulls from other GPUs or
+            # writes to the origin's GPU, at the measured 770 GB/s peer rate;
+            # overlapped, only the last sub-slice's share is exposed
+            from paper_2510_08874_b200.replicas import _ReduceOverlap
+            ovl = _ReduceOverlap(A, B, C, cfg)
+            ingress = [0] * p
+            last = [0] * p
+            for t, subs in ovl.subs.items():
+                cols = C.segment(t, 0).cols
+                for k_, (r0, r1, rep) in enumerate(subs):
+                    red_rank = C.owner_rank(t, rep)
+                    nb = (r1 - r0) * cols * 4
+                    remote = sum(1 for r in range(C.c) if C.owner_rank(t, r) != red_rank) * nb
+                    remote += nb if C.owner_rank(t, 0) != red_rank else 0     # write-back into the origin
+                    ingress[red_rank] += remote
+                    last[red_rank] = remote
+            solo["k4_nvlink_ms_model"] = max(ingress) / 770e9 * 1e3
+            solo["k4_exposed_ms_model"] = max(last) / 770e9 * 1e3
+        gbps = float(os.environ.get("UM_GET_GBPS", "0") or 0)
+        solo["pulls_paced_gbps"] = gbps or None
+        t_gpu = max(per_k1) + solo.get("k4_exposed_ms_model", 0.0)
+        solo["projected_ms_per_gpu"] = t_gpu
+        solo["projected_tflops_per_gpu"] = flops / p / (t_gpu * 1e-3) / 1e12
     out = {"config": name, "p": p, "stationarity": stationarity.value if hasattr(stationarity, "value") else str(stationarity),
            "m": m, "n": n, "k": k, "partitions": [ap, bp, cp], "replication": [ca, cb, cc],
            "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12,
@@ -125,7 +155,10 @@ def main():
                 so = r["solo"]
                 print(f"    solo ranks: max {so['rank_ms_max']:.3f} ms/rank -> per-GPU "
                       f"{min(so['per_gpu_tflops_ranks']):.0f}..{max(so['per_gpu_tflops_ranks']):.0f} TFLOP/s; "
-                      f"K4 reduce (all slices on this GPU) {so['reduce_ms_all_slices']:.3f} ms", flush=True)
+                      f"K4 reduce (all slices on this GPU) {so['reduce_ms_all_slices']:.3f} ms; projected "
+                      f"{so['projected_tflops_per_gpu']:.0f} TFLOP/s per GPU "
+                      f"(pulls paced at {so['pulls_paced_gbps']} GB/s, K4 exposed "
+                      f"{so.get('k4_exposed_ms_model', 0):.3f} ms)", flush=True)
     if a.json:
         with open(a.json, "w") as f:
             json.dump({"peak_tflops": peak, "rows": rows}, f, indent=1)

@@ -14,7 +14,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 engine = sys.argv[3] if len(sys.argv) > 3 else "kernel"
 extra = {k: (int(v) if v.isdigit() else v) for k, v in (kv.split("=", 1) for kv in sys.argv[4:])}
-extra = {k: (bool(v) if k in ("chain_order", "overlap_reduce", "fused_accumulate") else v) for k, v in extra.items()}
+extra = {k: (bool(v) if k in ("chain_order", "overlap_reduce", "fused_accumulate", "fine_waits") else v) for k, v in extra.items()}
 m, n, k, ap, bp, cp, fa, fb, fc, desc = bench.CONFIGS[name]
 fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, fa(p), fb(p), fc(p), seed=0, real=True, synthetic=True,
                                    devices=[0])

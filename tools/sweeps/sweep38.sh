@@ -1,0 +1,3 @@
+timeout 120 python tools/get_probe.py 2>&1 | grep -v CUDAEvent.h | grep "512 MiB) in-kernel"
+UM_GET_GBPS=770 timeout 120 python tools/get_probe.py 2>&1 | grep -v CUDAEvent.h | grep "512 MiB) in-kernel\|both"
+UM_GET_GBPS=770 timeout 1200 python tools/bench_matrix.py --configs cfg2,cfg3,cfg4,cfg5 --ps 2,4,8 --json gpurun_out/matrix_paced.json 2>&1 | grep -v CUDAEvent.h
