@@ -30,6 +30,31 @@ from paper_2510_08874_b200 import runtime as rt  # noqa: E402
 from paper_2510_08874_b200.cli import build_problem  # noqa: E402
 
 
+def k4_nvlink_model(C, ovl, link_gbs: float = 770.0):
+    """K4 over NVLink (model): per reducer, the bytes it reads from other GPUs
+    (non-local replicas, and the origin when remote) and writes to the origin
+    when remote, at the measured 770 GB/s per direction (full duplex: the
+    slower direction counts).  Returns (whole reduction, last sub-slice) in ms
+    for the busiest reducer: overlapped with the GEMMs, only the last
+    sub-slice's share is exposed."""
+    p = C.fabric.nprocs
+    rd, wr = [0] * p, [0] * p
+    last = [0.0] * p
+    for t, subs in ovl.subs.items():
+        cols = C.segment(t, 0).cols
+        for r0, r1, rep in subs:
+            red = C.owner_rank(t, rep)
+            nb = (r1 - r0) * cols * 4
+            origin_remote = C.owner_rank(t, 0) != red
+            reads = sum(1 for r in range(1, C.c) if C.owner_rank(t, r) != red) * nb + (nb if origin_remote else 0)
+            writes = nb if origin_remote else 0
+            rd[red] += reads
+            wr[red] += writes
+            last[red] = max(reads, writes)
+    whole = max(max(a, b) for a, b in zip(rd, wr))
+    return whole / (link_gbs * 1e9) * 1e3, max(last) / (link_gbs * 1e9) * 1e3
+
+
 def run_one(name, p, steps, warmup, stationarity, extra):
     m, n, k, ap, bp, cp, fa, fb, fc, desc = bench.CONFIGS[name]
     ca, cb, cc = fa(p), fb(p), fc(p)
@@ -96,19 +121,9 @@ def run_one(name, p, steps, warmup, stationarity, extra):
             # overlapped, only the last sub-slice's share is exposed
             from paper_2510_08874_b200.replicas import _ReduceOverlap
             ovl = _ReduceOverlap(A, B, C, cfg)
-            ingress = [0] * p
-            last = [0] * p
-            for t, subs in ovl.subs.items():
-                cols = C.segment(t, 0).cols
-                for k_, (r0, r1, rep) in enumerate(subs):
-                    red_rank = C.owner_rank(t, rep)
-                    nb = (r1 - r0) * cols * 4
-                    remote = sum(1 for r in range(C.c) if C.owner_rank(t, r) != red_rank) * nb
-                    remote += nb if C.owner_rank(t, 0) != red_rank else 0     # write-back into the origin
-                    ingress[red_rank] += remote
-                    last[red_rank] = remote
-            solo["k4_nvlink_ms_model"] = max(ingress) / 770e9 * 1e3
-            solo["k4_exposed_ms_model"] = max(last) / 770e9 * 1e3
+            whole, last = k4_nvlink_model(C, ovl)
+            solo["k4_nvlink_ms_model"] = whole
+            solo["k4_exposed_ms_model"] = last
         gbps = float(os.environ.get("UM_GET_GBPS", "0") or 0)
         solo["pulls_paced_gbps"] = gbps or None
         t_gpu = max(per_k1) + solo.get("k4_exposed_ms_model", 0.0)
