@@ -1,5 +1,5 @@
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from tools.gemm_probe import run
 which = sys.argv[1]
 offs = {"rows": (5, 0, 7, 0, 2, 0), "acol8": (0, 8, 0, 0, 0, 0), "acol3": (0, 3, 0, 0, 0, 0),

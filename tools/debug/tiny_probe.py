@@ -1,5 +1,5 @@
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 from paper_2510_08874_b200 import kernels
 torch.cuda.init(); torch.zeros(1, device="cuda"); torch.cuda.synchronize()
