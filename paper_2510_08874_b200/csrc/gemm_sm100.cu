@@ -109,6 +109,7 @@ struct alignas(16) Work {
   int32_t slot;               // completion-signal slot (-1: none)
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
   int32_t a_fine, b_fine;     // 1-based get whose chunks A (per tile rows) / B (per k-block rows) wait for
+  int32_t c_prefetch, pad2_;  // > 0: prefetch this tile's C into L2 that many k-blocks before its epilogue
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -343,6 +344,9 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
         tile_coords(works[w0], t - works[w0].tile_start, mb, nb);
         // a k-chain: the segments (ops with the same C region) are loaded one
         // after the other into the same accumulator, one epilogue per tile
+        int kbg = 0;   // k-block index over the whole chain (C prefetch trigger)
+        const int cpf_at = works[w0].c_prefetch > 0 && works[w0].c_remote == 0
+                               ? max(0, works[w0].num_kb - works[w0].c_prefetch) : -1;
         for (int w = w0; w < w0 + works[w0].nseg; ++w) {
         const Work& wk = works[w];
         // fused get -> GEMM: this segment reads operand slices a get is still
@@ -383,6 +387,14 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           const int kcol = wk.a_col0 + kb * BK;
           const int krow = wk.b_row0 + kb * BK;
           if (wk.b_fine) wait_rows(wk.b_fine - 1, krow, krow + BK);   // this k-block's B rows
+          if (kbg++ == cpf_at) {
+            // bring this CTA's 128 x NT block of C into L2 ahead of the reduce-adds
+            const Work& hd = works[w0];
+            const CUtensorMap* mcp = &maps[3 * w0 + 2];
+            const int crow = hd.c_row0 + mb * BM * CG + (int)cta_rank * BM;
+            for (int r = 0; r < BM; r += 32)
+              for (int c = 0; c < NT; c += 32) ptx::tma_prefetch_2d(mcp, hd.c_col0 + nb * NT + c, crow + r);
+          }
           if constexpr (CG == 1) {
             ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pa);
           } else {
@@ -783,6 +795,7 @@ struct Knobs {
   int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 0, sched_static = 0;
   int epi_warps = 4;
   int chain = 1;
+  int cpf = 0;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -799,6 +812,7 @@ static const Knobs& knobs() {
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
+    k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
   });
   return k;
 }
@@ -1057,6 +1071,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.wait_flag = op.wait_flag;
     w.wait_value = op.wait_value;
     w.wait_mask = op.get_mask;
+    w.c_prefetch = kn.cpf;
     w.a_fine = op.a_get;
     w.b_fine = op.b_get;
     w.group = kn.group;
