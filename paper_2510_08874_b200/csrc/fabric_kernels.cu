@@ -1,6 +1,9 @@
-// K2-K5: one-sided data movement for the distributed GEMM.
+// K2'-K5: one-sided data movement for the distributed GEMM (the default K2
+// pulls run inside the K1 launch, gemm_sm100.cu; um_get is the copy-engine form).
 //
 //  um_get             <- Fabric.get / get_async        (fabric.py:156-192)
+//  um_signal / um_wait_geq <- PendingCopy.wait / the run-level barrier, as
+//                        stream memory operations (no SM held)
 //  um_accumulate      <- Fabric.accumulate PEER_ATOMIC (fabric.py:203-234)
 //  um_reduce_replicas <- DistributedMatrix.reduce_replicas (distmatrix.py:211-232)
 //  um_copy            <- DistributedMatrix.broadcast_replica (distmatrix.py:234-250)

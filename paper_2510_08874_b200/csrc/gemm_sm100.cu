@@ -8,9 +8,23 @@
 //   fabric.accumulate PEER_ATOMIC (fabric.py:203-234) via distmatrix.accumulate_tile
 // into the epilogue.
 //
+// and, in the same launch, the one-sided gets of run_direct
+//   distmatrix.get_tile_async -> fabric.get_async (distmatrix.py:161-168,
+//   fabric.py:177-201), PendingTileCopy.wait before local_gemm (runtime.py:219-236)
+// as get warps that pull remote slices while the tensor cores work.
+//
 // Design (B200-first):
 //  * warp-specialised persistent kernel: warp 0 = TMA producer, warp 1 = MMA
-//    issuer (one thread issues tcgen05.mma), warps 2..5 = epilogue.
+//    issuer (one thread issues tcgen05.mma), warps 2..5 = epilogue, warps
+//    6..9 = get engine (pull chunks of remote slices into a staging pool; the
+//    producer waits per band, per tile rows of A or per k-block rows of B).
+//  * a dynamic tile scheduler (atomic counter, tile queue broadcast to both
+//    CTAs of a pair) hands out tiles in raster order over the launch's ops.
+//  * ops with the same C region form a k-chain: their k-segments accumulate
+//    in one TMEM accumulator and the tile is reduced into C once.
+//  * completion signals: when all tiles of the ops naming a done_flag are in
+//    C, the epilogue adds their count to the flag (red.release.sys), which a
+//    replica reducer's stream waits on (overlapped K4).
 //  * operands are consumed IN PLACE from strided tile slices: each operand's
 //    TMA tensor map is based at the tile base with dims (col_hi,row_hi) and the
 //    loads start at (col_lo,row_lo), so arbitrary row offsets and ragged edges
@@ -29,8 +43,8 @@
 //  * epilogue: tcgen05.ld -> registers -> swizzled smem -> TMA reduce-add
 //    (cp.reduce.async.bulk.tensor ... add) into the local C tile, or
 //    red.global.add.v4.f32 straight into a peer C tile (fused K3).
-//  * L2: tiles are walked in groups of m-tiles so a wave of clusters shares A
-//    and B panels; per-operand eviction hints are available as knobs.
+//  * L2: tiles are walked in groups of 4 n-tiles so a wave of clusters shares
+//    A and B panels; per-operand eviction hints are available as knobs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
