@@ -366,7 +366,7 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     d2h = nbytes(C, replica0_only=True)
 
     def step():
-        multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels)
+        multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, copy_streams=args.copy_streams)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -381,7 +381,7 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     ms = max_over_ranks(e0.elapsed_time(e1) / steps)
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "api": "hostio.multiply_from_host",
-            "panels": args.panels}
+            "panels": args.panels, "copy_streams": args.copy_streams}
 
 
 def main():
@@ -393,6 +393,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--panels", type=int, default=32, help="row panels of the host-streaming e2e path")
+    ap.add_argument("--copy-streams", type=int, default=1, help="copy streams per direction in the e2e path (measured: 1 best)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="target seconds per reference-arm step")
