@@ -580,6 +580,26 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           __syncwarp();
           const int c4 = lane & 7;          // 16-byte column group of this lane
           const int col = col0 + 4 * c4;
+          if (wk.c_remote == 4 && wk.c_vec_ok && col0 + 32 <= wk.n && row_in_op + 32 <= wk.m) {
+            // exclusive writer: plain read-modify-write through the load/store
+            // units (the TMA unit stays free for the producer's operand loads);
+            // 8 independent 16-byte loads in flight per lane
+            float4 cv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + (lane >> 3);
+              cv[i] = *reinterpret_cast<const float4*>(wk.c_ptr + (int64_t)(wk.c_row0 + row_in_op + rr) * wk.c_pitch +
+                                                       wk.c_col0 + col);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + (lane >> 3);
+              const float4 v = ptx::ld_shared_v4f(base + rr * 128 + ((c4 ^ (rr & 7)) << 4));
+              cv[i].x += v.x; cv[i].y += v.y; cv[i].z += v.z; cv[i].w += v.w;
+              *reinterpret_cast<float4*>(wk.c_ptr + (int64_t)(wk.c_row0 + row_in_op + rr) * wk.c_pitch + wk.c_col0 +
+                                         col) = cv[i];
+            }
+          } else
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = i * 4 + (lane >> 3);   // row within the warp's 32
@@ -1092,6 +1112,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
       if (dbg && !strcmp(dbg, "store")) w.c_remote = 2;
       if (dbg && !strcmp(dbg, "none")) w.c_remote = 3;
       if (dbg && !strcmp(dbg, "red")) w.c_remote = 1;  // coalesced red.global epilogue for local C
+      if (dbg && !strcmp(dbg, "rmw")) w.c_remote = 4;  // exclusive-writer load/add/store epilogue
     }
     w.a_row0 = (int32_t)op.a.row_lo;
     w.a_col0 = (int32_t)op.a.col_lo;
