@@ -84,3 +84,28 @@ def test_fullsize_exact(cuda, name, p):
     # checksum of checksums over all of C
     expect = float(torch.dot(_col_sums(A), _row_sums(B)).item())
     assert _total(C) == expect, (name, p)
+
+
+@pytest.mark.parametrize("p", [1, 8])
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_fullsize_real_inputs_within_tolerance(cuda, name, p):
+    """Real uniform(-1, 1) inputs rounded to bf16 (as the north star states), fp32
+    accumulation over k up to 65536 (cfg3): sampled entries of C against the fp64
+    product of the same bf16 values, max_ij |dC| / (|A_i,:| |B_:,j|) <= 1e-5 (the
+    north-star bar is 1e-3; k-chains and split reductions only reorder fp32 adds)."""
+    m, n, k, ap, bp, cp, fa, fb, fc = CONFIGS[name]
+    fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, fa(p), fb(p), fc(p), seed=SEED, synthetic=True,
+                                       real=True)
+    execute_multiply(A, B, C, ExecConfig())
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(sum(map(ord, name)) * 7 + p)
+    rows = sorted(set(rng.integers(0, m, 30).tolist()) | {0, m - 1})
+    cols = sorted(set(rng.integers(0, n, 30).tolist()) | {0, n - 1})
+    a_rows = np.concatenate([O.round_bf16(O.fill_values(SEED, r, r + 1, 0, k, "real")) for r in rows]).astype(np.float64)
+    b_cols = np.concatenate([O.round_bf16(O.fill_values(SEED + 1, 0, k, c, c + 1, "real")) for c in cols],
+                            axis=1).astype(np.float64)
+    ref = a_rows @ b_cols
+    got = _entries(C, rows, cols)
+    norm = np.linalg.norm(a_rows, axis=1)[:, None] * np.linalg.norm(b_cols, axis=0)[None, :]
+    err = float(np.max(np.abs(got - ref) / norm))
+    assert err <= 1e-5, (name, p, err)
