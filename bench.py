@@ -195,31 +195,111 @@ def cpu_oracle_rate(m, n, k, p, desc, target_s: float):
     return flops / dt / 1e12, f"{rows}x{n}x{k} row sample of {desc} (fp64 numpy oracle port)", cores, dt
 
 
+_REF = {}   # fork-shared operands of the reference-kernel pool
+
+
+def _ref_worker(i):
+    """One host core: the reference's compiled local GEMM (_gemmcore.pyx:10-25)
+    on row block i of the sample."""
+    import numpy as np
+
+    mod = ref_gemm_module()
+    a, b, rpc = _REF["a"], _REF["b"], _REF["rpc"]
+    c = np.zeros((rpc, b.shape[1]))
+    t0 = time.perf_counter()
+    mod.gemm_accumulate(a[i * rpc:(i + 1) * rpc], b, c)
+    return time.perf_counter() - t0
+
+
+def ref_gemm_module():
+    """The reference's own compiled kernel, built from its sources into oracle/_ref
+    (oracle/Makefile), or None when it is not there."""
+    d = os.path.join(ROOT, "oracle", "_ref")
+    if d not in sys.path:
+        sys.path.insert(0, d)
+    try:
+        import _gemmcore  # noqa: PLC0415
+
+        return _gemmcore
+    except ImportError:
+        return None
+
+
+class RefKernelPool:
+    """The reference's CPU path on cfg's local GEMM (at p = 1 the whole multiply
+    is one `local_gemm`, runtime.py:96-107, on the compiled backend the
+    reference selects when built: kernels.py:20-28), on every host core: the
+    kernel holds the GIL, so one forked process per core, each on its own row
+    block of a row sample (fp64, as the reference)."""
+
+    def __init__(self, n, k, target_s):
+        import multiprocessing as mp
+
+        import numpy as np
+
+        self.mod = ref_gemm_module()
+        self.cores = len(os.sched_getaffinity(0))
+        rng = np.random.default_rng(0)
+        b = rng.uniform(-1, 1, size=(k, n))
+        probe = rng.uniform(-1, 1, size=(4, k))
+        c = np.zeros((4, n))
+        t0 = time.perf_counter()
+        self.mod.gemm_accumulate(probe, b, c)
+        per_row = (time.perf_counter() - t0) / 4
+        rpc = max(1, int(target_s / per_row))
+        _REF.update(a=rng.uniform(-1, 1, size=(rpc * self.cores, k)), b=b, rpc=rpc)
+        self.rows = rpc * self.cores
+        self.n, self.k = n, k
+        self.pool = mp.get_context("fork").Pool(self.cores)
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        self.pool.map(_ref_worker, range(self.cores), chunksize=1)
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.pool.terminate()
+
+
 def reference_arm(args):
-    """--impl reference: the CPU oracle port on this host's cores (rank 0 only)."""
+    """--impl reference: the reference's own CPU implementation of the path on this
+    host's cores (its compiled kernel from oracle/_ref; the numpy oracle port if
+    that is absent), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     m, n, k, ap, bp, cp, fa, fb, fc, desc = CONFIGS[args.config]
-    import numpy as np
-
-    from oracle import um_oracle as O
-
-    cores = len(os.sched_getaffinity(0))
-    rate, sample, cores, dt = cpu_oracle_rate(m, n, k, args.gpus, desc, target_s=args.ref_step_s)
-    rows = int(sample.split("x")[0])
-    rng = np.random.default_rng(1)
-    a = rng.uniform(-1, 1, size=(rows, k))
-    b = rng.uniform(-1, 1, size=(k, n))
-    mats = [O.Mat("A", rows, k, O.Spec(rows, k, 1, 1), 1, 1), O.Mat("B", k, n, O.Spec(k, n, 1, 1), 1, 1),
-            O.Mat("C", rows, n, O.Spec(rows, n, 1, 1), 1, 1)]
-    with blas_threads(cores):
+    if ref_gemm_module() is not None:
+        pool = RefKernelPool(n, k, args.ref_step_s)
         for _ in range(args.warmup):
-            O.execute("c", *mats, a, b)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            O.execute("c", *mats, a, b)
-        dt = (time.perf_counter() - t0) / args.steps
+            pool.step()
+        dts = [pool.step() for _ in range(args.steps)]
+        pool.close()
+        dt = sum(dts) / len(dts)
+        rows, cores, kind = pool.rows, pool.cores, "reference"
+        sample = (f"{rows}x{n}x{k} row sample of {desc}: the reference's compiled _gemmcore kernel "
+                  f"(oracle/_ref, fp64), one process per core")
+    else:
+        import numpy as np
+
+        from oracle import um_oracle as O
+
+        cores = len(os.sched_getaffinity(0))
+        _, sample, cores, _ = cpu_oracle_rate(m, n, k, args.gpus, desc, target_s=args.ref_step_s)
+        rows = int(sample.split("x")[0])
+        rng = np.random.default_rng(1)
+        a = rng.uniform(-1, 1, size=(rows, k))
+        b = rng.uniform(-1, 1, size=(k, n))
+        mats = [O.Mat("A", rows, k, O.Spec(rows, k, 1, 1), 1, 1), O.Mat("B", k, n, O.Spec(k, n, 1, 1), 1, 1),
+                O.Mat("C", rows, n, O.Spec(rows, n, 1, 1), 1, 1)]
+        with blas_threads(cores):
+            for _ in range(args.warmup):
+                O.execute("c", *mats, a, b)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                O.execute("c", *mats, a, b)
+            dt = (time.perf_counter() - t0) / args.steps
+        kind = "port"
     val = 2.0 * rows * n * k / dt / 1e12
     out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -227,8 +307,7 @@ def reference_arm(args):
            "config": {"workload": f"{args.config}: {desc}", "m": m, "n": n, "k": k, "p": args.gpus,
                       "partitions": [ap, bp, cp], "sample_rows": rows},
            "impl": "reference",
-           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                            "sample": sample},
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": kind, "sample": sample},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -314,8 +393,19 @@ def b200_arm(args):
     # ---- CPU baseline (oracle port) on rank 0, N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, sample, cores, _ = cpu_oracle_rate(m, n, k, p, desc, target_s=args.cpu_s)
-        cpu = {"value": rate, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample}
+        port_rate, port_sample, cores, _ = cpu_oracle_rate(m, n, k, p, desc, target_s=args.cpu_s / 2)
+        if ref_gemm_module() is not None:
+            pool = RefKernelPool(n, k, args.cpu_s / 2)
+            pool.step()
+            dt = pool.step()
+            pool.close()
+            cpu = {"value": 2.0 * pool.rows * n * k / dt / 1e12, "unit": "TFLOP/s", "cores": pool.cores,
+                   "kind": "reference",
+                   "sample": f"{pool.rows}x{n}x{k} row sample of {desc}: the reference's compiled _gemmcore "
+                             f"kernel (oracle/_ref, fp64), one process per core",
+                   "numpy_port": {"value": port_rate, "cores": cores, "sample": port_sample}}
+        else:
+            cpu = {"value": port_rate, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": port_sample}
 
     traffic = k1_traffic(args.config) if world == 1 else None
     # A read once, B read once, C read + written once (fp32 C += A.B), per K1 launch
