@@ -75,7 +75,8 @@ constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 #define UM_GET_WARPS 4
 #endif
 constexpr int GET_WARPS = UM_GET_WARPS;
-constexpr int num_threads(int ew) { return 64 + ew * 32 + GET_WARPS * 32; }
+// launches without pulls are instantiated without get warps (GW = 0)
+constexpr int num_threads(int ew, int gw) { return 64 + ew * 32 + gw * 32; }
 // default rasterisation group: 4 n-tiles (negative = group along n), i.e. a
 // 4-panel slice of B stays hot while A streams; measured best of {-4,4,8,16,32}
 // on cfg2 / 16384^3 / cfg3 shapes with the dynamic scheduler. UM_GEMM_GROUP overrides.
@@ -83,10 +84,10 @@ constexpr int GROUP_M = -4;
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
 
-template <int CG, int NT, int EW = 4>
+template <int CG, int NT, int EW = 4, int GW = GET_WARPS>
 struct Cfg {
   static constexpr int EPI_WARPS = EW;
-  static constexpr int NUM_THREADS = num_threads(EW);
+  static constexpr int NUM_THREADS = num_threads(EW, GW);
   static constexpr int EPI_BOXES = EW == 4 ? 2 : 1;           // smem boxes per epilogue warp
   static constexpr int NACC = NT / UMMA_N;                   // accumulators per tile
   static constexpr int NBUF = 2 / NACC;                      // TMEM tile buffers
@@ -205,6 +206,8 @@ struct alignas(64) LaunchArgs {
   int ngets, total_chunks;
   int nslots;
   uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
+  unsigned long long* prof;   // (profiling, UM_GEMM_STALLS) per cluster: MMA-thread cycles total / waiting
+                              // for operands / for the epilogue to free TMEM / for the next tile
   SignalSlot slots[MAX_SLOTS];
   CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
   Work inl_works[MAX_INLINE_OPS];
@@ -212,10 +215,10 @@ struct alignas(64) LaunchArgs {
 };
 static_assert(sizeof(LaunchArgs) <= 32764, "kernel parameter block");
 
-template <int CG, int NT, int EW>
-__global__ void __launch_bounds__(num_threads(EW), 1)
+template <int CG, int NT, int EW, int GW>
+__global__ void __launch_bounds__(num_threads(EW, GW), 1)
     gemm_bf16_kernel(const __grid_constant__ LaunchArgs args) {
-  using C = Cfg<CG, NT, EW>;
+  using C = Cfg<CG, NT, EW, GW>;
   constexpr int EPI_WARPS = EW;
   // small op lists travel inside the kernel parameters (no per-launch device
   // allocation or host->device copy); larger ones in a global-memory block
@@ -435,6 +438,17 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      unsigned long long c_full = 0, c_tmem = 0, c_tile = 0;
+      const unsigned long long c_begin = clock64();
+      auto timed = [&](unsigned long long& acc, auto&& fn) {
+        if (args.prof) {
+          const unsigned long long t0 = clock64();
+          fn();
+          acc += clock64() - t0;
+        } else {
+          fn();
+        }
+      };
       // all MMAs of one k-block into accumulator `acc_col`
       auto issue = [&](int stg, uint32_t acc_col, int j, bool first_kb) {
         const uint32_t sa = ptx::smem_u32(smem_a + stg * C::A_BYTES);
@@ -450,17 +464,18 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
         }
       };
       for (;; ++it) {
-        const int t = next_tile(it);
+        int t = 0;
+        timed(c_tile, [&] { t = next_tile(it); });
         if (t >= total_tiles) break;
         const int w = find_work(works, nwork, t);
         const int num_kb = works[w].num_kb;
         const int buf = it % C::NBUF;
         const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
         if constexpr (C::NACC == 1) {
-          ptx::mbar_wait(&tmem_empty[buf], tph ^ 1);
+          timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[buf], tph ^ 1); });
           ptx::tc_fence_after();
           for (int kb = 0; kb < num_kb; ++kb) {
-            ptx::mbar_wait(&full[stage], phase);
+            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
             issue(stage, buf * UMMA_N, 0, kb == 0);
             ptx::umma_commit<CG>(&empty[stage], 0x3);
@@ -469,16 +484,16 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
         } else {
           // accumulator 0 runs ahead by D k-blocks while the epilogue drains accumulator 1
           const int D = min(C::STAGES - 1, num_kb);
-          ptx::mbar_wait(&tmem_empty[0], tph ^ 1);
+          timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[0], tph ^ 1); });
           ptx::tc_fence_after();
           const int stage0 = stage;
           for (int kb = 0; kb < D; ++kb) {
-            ptx::mbar_wait(&full[stage], phase);
+            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
             issue(stage, 0, 0, kb == 0);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::mbar_wait(&tmem_empty[1], tph ^ 1);
+          timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[1], tph ^ 1); });
           ptx::tc_fence_after();
           int st = stage0;
           for (int kb = 0; kb < D; ++kb) {
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           // accumulator 1's tail
           const int E = works[0].no_end_stagger ? 0 : min(C::STAGES - 1, num_kb - D);
           for (int kb = D; kb < num_kb - E; ++kb) {
-            ptx::mbar_wait(&full[stage], phase);
+            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
             issue(stage, 0, 0, false);
             issue(stage, UMMA_N, 1, false);
@@ -499,7 +514,7 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           }
           const int stageE = stage;
           for (int kb = num_kb - E; kb < num_kb; ++kb) {
-            ptx::mbar_wait(&full[stage], phase);
+            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
             issue(stage, 0, 0, false);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -514,6 +529,13 @@ __global__ void __launch_bounds__(num_threads(EW), 1)
           ptx::umma_commit<CG>(&tmem_full[1], 0x3);
         }
         if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
+      }
+      if (args.prof) {
+        unsigned long long* o = args.prof + 4 * (blockIdx.x / CG);
+        o[0] = clock64() - c_begin;
+        o[1] = c_full;
+        o[2] = c_tmem;
+        o[3] = c_tile;
       }
     }
   } else if (warp < 2 + EW) {
@@ -870,14 +892,14 @@ static int* stream_counters(int device, cudaStream_t stream) {
   return p;
 }
 
-template <int CG, int NT, int EW>
+template <int CG, int NT, int EW, int GW>
 static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
-  using C = Cfg<CG, NT, EW>;
+  using C = Cfg<CG, NT, EW, GW>;
   const int total_tiles = args.total_tiles;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
   if (!attr_set[device]) {
-    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT, EW, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES));
     attr_set[device] = true;
   }
@@ -897,7 +919,7 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW>, args));
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW, GW>, args));
   return UM_OK;
 }
 
@@ -1293,10 +1315,43 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   }
   if (P->nslots)
     UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 3 + MAX_GETS, 0, P->nslots * sizeof(int), stream));
-  if (P->CG == 1) return launch<1, 256, 4>(args, P->device, stream);
-  if (P->NT == 512)
-    return P->EW == 8 ? launch<2, 512, 8>(args, P->device, stream) : launch<2, 512, 4>(args, P->device, stream);
-  return P->EW == 8 ? launch<2, 256, 8>(args, P->device, stream) : launch<2, 256, 4>(args, P->device, stream);
+  // profiling (UM_GEMM_STALLS=1): MMA-thread stall breakdown, synchronous, printed to stderr
+  static const bool stalls = env_int("UM_GEMM_STALLS", 0) != 0;
+  unsigned long long* prof = nullptr;
+  if (stalls) {
+    UM_CUDA_CHECK(cudaMallocAsync(&prof, 4 * 512 * sizeof(unsigned long long), stream));
+    UM_CUDA_CHECK(cudaMemsetAsync(prof, 0, 4 * 512 * sizeof(unsigned long long), stream));
+  }
+  args.prof = prof;
+  int rc;
+  const bool g = P->ngets > 0;
+  if (P->CG == 1) rc = g ? launch<1, 256, 4, GET_WARPS>(args, P->device, stream) : launch<1, 256, 4, 0>(args, P->device, stream);
+  else if (P->NT == 512 && P->EW == 8)
+    rc = g ? launch<2, 512, 8, GET_WARPS>(args, P->device, stream) : launch<2, 512, 8, 0>(args, P->device, stream);
+  else if (P->NT == 512)
+    rc = g ? launch<2, 512, 4, GET_WARPS>(args, P->device, stream) : launch<2, 512, 4, 0>(args, P->device, stream);
+  else if (P->EW == 8)
+    rc = g ? launch<2, 256, 8, GET_WARPS>(args, P->device, stream) : launch<2, 256, 8, 0>(args, P->device, stream);
+  else
+    rc = g ? launch<2, 256, 4, GET_WARPS>(args, P->device, stream) : launch<2, 256, 4, 0>(args, P->device, stream);
+  args.prof = nullptr;
+  if (prof) {
+    std::vector<unsigned long long> h(4 * 512);
+    cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaFreeAsync(prof, stream);
+    double tot = 0, full = 0, tmem = 0, tile = 0;
+    int n = 0;
+    for (int c = 0; c < 512; ++c)
+      if (h[4 * c]) {
+        tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += h[4 * c + 3]; ++n;
+      }
+    if (n)
+      fprintf(stderr, "[um_gemm stalls] %d clusters, MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
+                      "%.1f %%, for the next tile %.1f %% of %.0f cycles\n", n, 100 * full / tot, 100 * tmem / tot,
+              100 * tile / tot, tot / n);
+  }
+  return rc;
 }
 
 int launch_batch(const um_gemm_op* ops, int nops, const um_get_desc* gets, int ngets, int device,
