@@ -483,7 +483,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           }
         } else {
           // accumulator 0 runs ahead by D k-blocks while the epilogue drains accumulator 1
-          const int D = min(C::STAGES - 1, num_kb);
+          // no_end_stagger == 2: no stagger at all (both accumulators per k-block)
+          const int D = works[0].no_end_stagger == 2 ? 0 : min(C::STAGES - 1, num_kb);
           timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[0], tph ^ 1); });
           ptx::tc_fence_after();
           const int stage0 = stage;
@@ -507,8 +508,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           for (int kb = D; kb < num_kb - E; ++kb) {
             timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
-            issue(stage, 0, 0, false);
-            issue(stage, UMMA_N, 1, false);
+            issue(stage, 0, 0, kb == 0);          // kb == 0 only without a leading stagger (D == 0)
+            issue(stage, UMMA_N, 1, kb == 0);
             ptx::umma_commit<CG>(&empty[stage], 0x3);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
@@ -1159,7 +1160,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.c_pol = kn.cpol >= 0 && kn.cpol <= 2 ? kn.cpol : -1;
     w.prefetch = kn.prefetch;
     w.sched_static = kn.sched_static;
-    w.no_end_stagger = env_int("UM_GEMM_NO_END_STAGGER", 0) ? 1 : 0;
+    w.no_end_stagger = std::min(2, std::max(0, env_int("UM_GEMM_NO_END_STAGGER", 0)));
     if (w.a_pol > 2) w.a_pol = 0;
     if (w.b_pol > 2) w.b_pol = 0;
     w.c_vec_ok = ((reinterpret_cast<uintptr_t>(op.c.base) & 15) == 0) && (op.c.pitch % 4 == 0) && (op.c.col_lo % 4 == 0);
