@@ -194,6 +194,11 @@ UM_API int um_gemm_prepare(const um_gemm_op* ops, int32_t nops, const um_get_des
 UM_API int um_gemm_launch(void* handle, void* stream);
 UM_API int um_gemm_destroy(void* handle);
 
+/* Cap the persistent grid of K1 launches on `device` to `max_clusters` CTA
+ * pairs (0 = no cap): ranks sharing one GPU then run their launches side by
+ * side instead of one after the other.  Read at launch time.               */
+UM_API int um_gemm_set_grid_limit(int32_t device, int32_t max_clusters);
+
 /* Tile/stage knobs of the GEMM (bench/profiling): returns 0 and fills.    */
 UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages, int32_t* cta_group);
 

@@ -96,6 +96,7 @@ _SIGS = {
                                        ctypes.c_int32, _P(ctypes.c_void_p)]),
     "um_gemm_launch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "um_gemm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "um_gemm_set_grid_limit": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32]),
     "um_gemm_config": (ctypes.c_int, [_P(ctypes.c_int32)] * 5),
     "um_get": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_signal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),

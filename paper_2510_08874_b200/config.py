@@ -48,6 +48,11 @@ class ExecConfig:
                          (A: its tile's rows; B: each k-block's rows) instead of
                          for the whole band, so the first tiles start as soon
                          as their first rows land.
+      share_sms          ranks co-resident on one GPU each get an equal share of
+                         its SMs for their K1 launches, which then run side by
+                         side (off: measured 10-25 % slower than whole-GPU
+                         launches one after the other, e.g. cfg3 p=8 1118 vs
+                         1415 TFLOP/s).
       chain_order        issue ops that write the same C region back to back
                          (K1 accumulates such a k-chain in TMEM and reduces
                          into C once per tile).
@@ -76,6 +81,7 @@ class ExecConfig:
     overlap_reduce: bool = True
     chain_order: bool = True
     fine_waits: bool = True
+    share_sms: bool = False
     reduce_panels: int = 4
     k_split: int = 0
 

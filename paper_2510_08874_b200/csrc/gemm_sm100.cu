@@ -49,6 +49,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -893,6 +894,10 @@ static int* stream_counters(int device, cudaStream_t stream) {
   return p;
 }
 
+static std::atomic<int> g_grid_limit[64];
+
+static int grid_limit(int device) { return (device >= 0 && device < 64) ? g_grid_limit[device].load() : 0; }
+
 template <int CG, int NT, int EW, int GW>
 static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   using C = Cfg<CG, NT, EW, GW>;
@@ -907,7 +912,11 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   int sms = 0;
   UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   // with in-kernel gets every SM joins (its get warps pull even when it gets no tile)
-  const int clusters = args.ngets > 0 ? sms / CG : std::min(total_tiles, sms / CG);
+  int clusters = args.ngets > 0 ? sms / CG : std::min(total_tiles, sms / CG);
+  // co-resident ranks share the device: cap each launch's persistent grid so
+  // their launches (and the pulls inside them) run side by side
+  const int cap = grid_limit(device);
+  if (cap > 0) clusters = std::max(1, std::min(clusters, cap));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
@@ -1415,6 +1424,12 @@ extern "C" int um_gemm_destroy(void* handle) {
     if (P->scratch || P->dbuf) cudaDeviceSynchronize();   // buffers may still be read by a launch
     um::gemm::release(P, nullptr);
   }
+  return UM_OK;
+}
+
+extern "C" int um_gemm_set_grid_limit(int32_t device, int32_t max_clusters) {
+  if (device < 0 || device >= 64) return um::fail(UM_EVALUE, "device index out of range");
+  um::gemm::g_grid_limit[device].store(std::max(0, max_clusters));
   return UM_OK;
 }
 

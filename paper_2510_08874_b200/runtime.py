@@ -276,6 +276,25 @@ def _cross_process(A, B, C, cfg: ExecConfig) -> bool:
     return cross
 
 
+def _share_sms(fab, ranks) -> dict:
+    """Ranks co-resident on one GPU split its SMs: each K1 launch gets an equal
+    share of the persistent grid, so their launches (and the pulls inside
+    them) overlap instead of queueing behind each other.  Returns the caps set."""
+    per_dev: dict = {}
+    for r in ranks:
+        d = fab.device_of(r)
+        per_dev[d] = per_dev.get(d, 0) + 1
+    caps = {}
+    lib = _capi.load()
+    for d, nr in per_dev.items():
+        if nr > 1:
+            sms = ctypes.c_int32(0)
+            _capi.check(lib.um_sm_count(d, ctypes.byref(sms)), "um_sm_count")
+            caps[d] = max(1, (sms.value // 2) // nr)
+            _capi.check(lib.um_gemm_set_grid_limit(d, caps[d]), "um_gemm_set_grid_limit")
+    return caps
+
+
 def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                      execution: str = "direct", machine=None, max_compute: int | None = None,
                      max_comm: int | None = None, threaded: bool = False) -> dict[int, RunStats]:
@@ -300,6 +319,7 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
     done = []
     if execution == "direct":
         runs = []
+        caps = _share_sms(fab, ranks) if cfg.share_sms else {}
         for r in ranks:
             sched = lower_direct(A, B, C, cfg, r)
             _count_reference_traffic(A, B, C, cfg, sched)
@@ -307,6 +327,8 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
             if ovl is not None:
                 run.signals, run.signals_key = ovl.signals_for(sched), ("ovl", id(ovl))
             runs.append(run.issue())
+        for dev in caps:
+            _capi.check(_capi.load().um_gemm_set_grid_limit(dev, 0), "um_gemm_set_grid_limit")
         for run in runs:
             run.stats.flops = int(fab.counters.flops[run.caller])
             results[run.caller] = run.stats
