@@ -125,7 +125,7 @@ struct alignas(16) Work {
   int32_t slot;               // completion-signal slot (-1: none)
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
   int32_t a_fine, b_fine;     // 1-based get whose chunks A (per tile rows) / B (per k-block rows) wait for
-  int32_t c_prefetch, pad2_;  // > 0: prefetch this tile's C into L2 that many k-blocks before its epilogue
+  int32_t c_prefetch, stagger;  // C L2 prefetch distance (k-blocks); accumulator stagger depth (0 = STAGES-1)
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         } else {
           // accumulator 0 runs ahead by D k-blocks while the epilogue drains accumulator 1
           // no_end_stagger == 2: no stagger at all (both accumulators per k-block)
-          const int D = works[0].no_end_stagger == 2 ? 0 : min(C::STAGES - 1, num_kb);
+          const int SG = works[0].stagger > 0 ? min(works[0].stagger, C::STAGES - 1) : C::STAGES - 1;
+          const int D = works[0].no_end_stagger == 2 ? 0 : min(SG, num_kb);
           timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[0], tph ^ 1); });
           ptx::tc_fence_after();
           const int stage0 = stage;
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           }
           // accumulator 0 also finishes E k-blocks early, so its drain overlaps
           // accumulator 1's tail
-          const int E = works[0].no_end_stagger ? 0 : min(C::STAGES - 1, num_kb - D);
+          const int E = works[0].no_end_stagger ? 0 : min(SG, num_kb - D);
           for (int kb = D; kb < num_kb - E; ++kb) {
             timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
@@ -854,6 +855,7 @@ struct Knobs {
   int epi_warps = 4;
   int chain = 1;
   int cpf = 0;
+  int stagger = 0;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -871,6 +873,7 @@ static const Knobs& knobs() {
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
+    k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
   });
   return k;
 }
@@ -1158,6 +1161,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.wait_value = op.wait_value;
     w.wait_mask = op.get_mask;
     w.c_prefetch = kn.cpf;
+    w.stagger = kn.stagger;
     w.a_fine = op.a_get;
     w.b_fine = op.b_get;
     w.group = kn.group;
