@@ -325,7 +325,11 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
             _count_reference_traffic(A, B, C, cfg, sched)
             run = _RankRun(A, B, C, cfg, sched, start)
             if ovl is not None:
-                run.signals, run.signals_key = ovl.signals_for(sched), ("ovl", id(ovl))
+                # computed once per schedule (the plan built from it is cached too)
+                memo = sched.__dict__.setdefault("signals_memo", {})
+                if id(ovl) not in memo:
+                    memo[id(ovl)] = ovl.signals_for(sched)
+                run.signals, run.signals_key = memo[id(ovl)], ("ovl", id(ovl))
             runs.append(run.issue())
         for dev in caps:
             _capi.check(_capi.load().um_gemm_set_grid_limit(dev, 0), "um_gemm_set_grid_limit")
