@@ -126,6 +126,7 @@ struct alignas(16) Work {
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
   int32_t a_fine, b_fine;     // 1-based get whose chunks A (per tile rows) / B (per k-block rows) wait for
   int32_t c_prefetch, stagger;  // C L2 prefetch distance (k-blocks); accumulator stagger depth (0 = STAGES-1)
+  int32_t debug_halfb, pad3_;   // profiling only: skip half of the B loads (wrong results)
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -216,11 +217,15 @@ struct alignas(64) LaunchArgs {
 };
 static_assert(sizeof(LaunchArgs) <= 32764, "kernel parameter block");
 
-template <int CG, int NT, int EW, int GW>
+template <int CG, int NT, int EW, int GW, int NP>
 __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     gemm_bf16_kernel(const __grid_constant__ LaunchArgs args) {
   using C = Cfg<CG, NT, EW, GW>;
   constexpr int EPI_WARPS = EW;
+  // NP pairs per cluster (NP == 2: a cluster of 4 CTAs computes a 512 x NT
+  // super-tile; the two pairs share the B k-panel through TMA multicast)
+  static_assert(NP == 1 || (NP == 2 && CG == 2), "B multicast needs CTA pairs");
+  constexpr int CS = CG * NP;   // cluster size
   // small op lists travel inside the kernel parameters (no per-launch device
   // allocation or host->device copy); larger ones in a global-memory block
   const Work* __restrict__ works = args.works ? args.works : args.inl_works;
@@ -245,14 +250,34 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t cta_rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
-  const bool leader = cta_rank == 0;
-  constexpr int TQ_CONSUMERS = (CG == 2 ? 1 : 0) /*peer producer*/ + 1 /*MMA*/ + EPI_WARPS * CG;
+  // NP == 2 launches with a preferred cluster of 4 and a regular one of 2: the
+  // hardware forms clusters of 4 where a GPC has room and pairs elsewhere, so
+  // the cluster size (cs) and the number of pairs in it (np) are runtime values
+  const uint32_t crank = (CS > 1) ? ptx::cluster_ctarank() : 0u;   // rank in the cluster
+  const int cs = NP == 2 ? (int)ptx::cluster_nctarank() : CS;       // this cluster's size
+  const int np = cs / CG;                                           // pairs in this cluster
+  const uint32_t cta_rank = crank % CG;                             // rank in the CTA pair
+  const int pair = (int)(crank / CG);
+  const bool leader = cta_rank == 0;                                // pair leader (issues the MMAs)
+  const bool cleader = crank == 0;                                  // cluster leader (takes tiles)
+  const int TQ_CONSUMERS = (cs - 1) /*peer producers*/ + np /*MMA*/ + EPI_WARPS * cs;
+  // tile-queue entries: the tile index, or for NP == 2 (tile << 1 | half) where
+  // a lone pair runs the two 256-row halves of a 512-row tile one after the other
+  auto decode = [&](int q, int& t, int& row_off) {
+    int sub = 0;
+    if constexpr (NP == 2) {
+      t = q >> 1;
+      sub = np == 2 ? pair : (q & 1);
+    } else {
+      t = q;
+    }
+    row_off = sub * BM * CG + (int)cta_rank * BM;   // this CTA's rows in the tile
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], np);   // every pair's MMAs release the stage (multicast B)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tmem_full[s], 1);
@@ -325,30 +350,36 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         ptx::fence_proxy_async_global();
       };
       int flag_ok = -1;      // highest work index whose external arrival flag has been observed
+      int q = 0;
       for (int i = 0;; ++i) {
-        int t;
-        if (leader) {
-          // take the next tile and publish it to both CTAs of the pair
+        if (cleader) {
+          // take the next tile and publish it to every CTA of the cluster
           const int slot = i % TQ;
           ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
-          t = works[0].sched_static ? (int)(blockIdx.x / CG) + i * (int)(gridDim.x / CG)  // A/B knob
-                                    : atomicAdd(tile_counter, 1);
-          if (t > total_tiles) t = total_tiles;
-          tq[slot] = t;
-          if constexpr (CG == 2) {
-            ptx::st_shared_cluster_u32((const void*)&tq[slot], 1, (uint32_t)t);
-            ptx::mbar_arrive_cluster(&tq_full[slot], 0);
-            ptx::mbar_arrive_cluster(&tq_full[slot], 1);
+          if (NP == 2 && np == 1 && (i & 1)) {
+            q += 1;   // second half of the tile taken at i - 1
+          } else {
+            int t = (NP == 1 && works[0].sched_static) ? (int)(blockIdx.x / CS) + i * (int)(gridDim.x / CS)  // A/B knob
+                                                       : atomicAdd(tile_counter, 1);
+            if (t > total_tiles) t = total_tiles;
+            q = NP == 2 ? t << 1 : t;
+          }
+          tq[slot] = q;
+          if constexpr (CS > 1) {
+            for (int r = 1; r < cs; ++r) ptx::st_shared_cluster_u32((const void*)&tq[slot], r, (uint32_t)q);
+            for (int r = 0; r < cs; ++r) ptx::mbar_arrive_cluster(&tq_full[slot], r);
           } else {
             ptx::mbar_arrive_cluster(&tq_full[slot], 0);
           }
         } else {
-          t = next_tile(i);
+          q = next_tile(i);
         }
+        int t, row_off;
+        decode(q, t, row_off);
         if (t >= total_tiles) {
           if (leader) {
-            // this cluster is done with the counter; the last one out re-zeroes
-            // it for the next launch on this stream
+            // this pair is done with the counter (its cluster leader took its
+            // last tile); the last pair out re-zeroes it for the next launch
             __threadfence();
             if (atomicAdd(&tile_counter[1], 1) == (int)(gridDim.x / CG) - 1) {
               atomicExch(&tile_counter[0], 0);
@@ -381,7 +412,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const CUtensorMap* ma = &maps[3 * w + 0];
         const CUtensorMap* mbm = &maps[3 * w + 1];
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
-        const int arow = wk.a_row0 + mb * BM * CG + (int)cta_rank * BM;
+        const int arow = wk.a_row0 + mb * BM * CG * NP + row_off;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
         if (wk.a_fine) wait_rows(wk.a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
@@ -399,7 +430,11 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         for (int kb = 0; kb < wk.seg_kb; ++kb) {
           if (pf > 0 && kb + pf < wk.seg_kb) prefetch(kb + pf);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+          // (profiling only, UM_GEMM_DEBUG_HALFB: wrong results) skip the second
+          // accumulator's B sub-tiles -> bound on what halving B traffic can buy
+          const bool halfb = NP == 1 && C::NACC == 2 && works[0].debug_halfb;
+          const bool mcast = NP == 2 && np == 2;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (halfb ? C::B_BYTES / 2 : 0)) * CG);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
           uint8_t* sb = smem_b + stage * C::B_BYTES;
           const int kcol = wk.a_col0 + kb * BK;
@@ -409,7 +444,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             // bring this CTA's 128 x NT block of C into L2 ahead of the reduce-adds
             const Work& hd = works[w0];
             const CUtensorMap* mcp = &maps[3 * w0 + 2];
-            const int crow = hd.c_row0 + mb * BM * CG + (int)cta_rank * BM;
+            const int crow = hd.c_row0 + mb * BM * CG * NP + row_off;
             for (int r = 0; r < BM; r += 32)
               for (int c = 0; c < NT; c += 32) ptx::tma_prefetch_2d(mcp, hd.c_col0 + nb * NT + c, crow + r);
           }
@@ -422,10 +457,21 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           for (int j = 0; j < C::NACC; ++j)
 #pragma unroll
             for (int s = 0; s < C::SUB_PER_ACC; ++s) {
-              uint8_t* dst = sb + (j * C::SUB_PER_ACC + s) * SUB_BYTES;
+              if (halfb && j == 1) continue;
+              const int qsub = j * C::SUB_PER_ACC + s;
+              uint8_t* dst = sb + qsub * SUB_BYTES;
               const int col = bcol + j * UMMA_N + s * 64;
-              if constexpr (CG == 1) ptx::tma_load_2d(dst, mbm, &full[stage], col, krow, pb);
-              else ptx::tma_load_2d_cg2(dst, mbm, &full[stage], col, krow, pb);
+              if (mcast) {
+                // the CTA of the other pair with the same pair rank needs the same
+                // B sub-tiles: each loads half of them into both (multicast)
+                if ((qsub * 2) / C::B_SUBS != pair) continue;
+                ptx::tma_load_2d_cg2_mc(dst, mbm, &full[stage], col, krow,
+                                        (uint16_t)((1u << crank) | (1u << (crank ^ CG))), pb);
+              } else if constexpr (CG == 1) {
+                ptx::tma_load_2d(dst, mbm, &full[stage], col, krow, pb);
+              } else {
+                ptx::tma_load_2d_cg2(dst, mbm, &full[stage], col, krow, pb);
+              }
             }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -436,6 +482,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     // ===================== MMA issuer (one thread, leader CTA) =====================
     if (leader && lane == 0) {
       constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 1);
+      // a stage is free once every pair sharing its B (multicast) has consumed it
+      const uint16_t EMPTY_MASK = np == 2 ? (uint16_t)0xF : (uint16_t)0x3;
+      const uint16_t PAIR_MASK = (uint16_t)(0x3u << (pair * CG));
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -465,8 +514,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
       };
       for (;; ++it) {
-        int t = 0;
+        int t = 0, row_off_unused;
         timed(c_tile, [&] { t = next_tile(it); });
+        decode(t, t, row_off_unused);
         if (t >= total_tiles) break;
         const int w = find_work(works, nwork, t);
         const int num_kb = works[w].num_kb;
@@ -479,7 +529,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
             ptx::tc_fence_after();
             issue(stage, buf * UMMA_N, 0, kb == 0);
-            ptx::umma_commit<CG>(&empty[stage], 0x3);
+            ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
         } else {
@@ -501,7 +551,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           int st = stage0;
           for (int kb = 0; kb < D; ++kb) {
             issue(st, UMMA_N, 1, kb == 0);
-            ptx::umma_commit<CG>(&empty[st], 0x3);
+            ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
           // accumulator 0 also finishes E k-blocks early, so its drain overlaps
@@ -512,7 +562,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             ptx::tc_fence_after();
             issue(stage, 0, 0, kb == 0);          // kb == 0 only without a leading stagger (D == 0)
             issue(stage, UMMA_N, 1, kb == 0);
-            ptx::umma_commit<CG>(&empty[stage], 0x3);
+            ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
           const int stageE = stage;
@@ -522,23 +572,23 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             issue(stage, 0, 0, false);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::umma_commit<CG>(&tmem_full[0], 0x3);
+          ptx::umma_commit<CG>(&tmem_full[0], PAIR_MASK);
           st = stageE;
           for (int kb = num_kb - E; kb < num_kb; ++kb) {
             issue(st, UMMA_N, 1, false);
-            ptx::umma_commit<CG>(&empty[st], 0x3);
+            ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
-          ptx::umma_commit<CG>(&tmem_full[1], 0x3);
+          ptx::umma_commit<CG>(&tmem_full[1], PAIR_MASK);
         }
-        if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], 0x3);
+        if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], PAIR_MASK);
       }
       if (args.prof) {
         unsigned long long* o = args.prof + 4 * (blockIdx.x / CG);
         o[0] = clock64() - c_begin;
         o[1] = c_full;
         o[2] = c_tmem;
-        o[3] = c_tile;
+        o[3] = c_tile | ((unsigned long long)cs << 56);   // + this cluster's size
       }
     }
   } else if (warp < 2 + EW) {
@@ -555,9 +605,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     int it = 0;
     int sbuf = 0;
     for (;; ++it) {
-      int t = 0;
+      int t = 0, row_off;
       if (lane == 0) t = next_tile(it);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      decode(__shfl_sync(0xffffffffu, t, 0), t, row_off);
       if (t >= total_tiles) break;
       const int w = find_work(works, nwork, t);
       const Work& wk = works[w];
@@ -567,7 +617,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       tile_coords(wk, t - wk.tile_start, mb, nb);
       const int buf = it % C::NBUF;
       const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
-      const int row_in_op = mb * BM * CG + (int)cta_rank * BM + q * 32;   // first row of this warp
+      const int row_in_op = mb * BM * CG * NP + row_off + q * 32;   // first row of this warp
 
       // one 32x32 fp32 chunk (lane = row) from registers into C
       auto emit = [&](const uint32_t (&r)[32], int col0) {
@@ -653,7 +703,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         if (lane == 0) {
           uint64_t* bar = &tmem_empty[C::NACC == 1 ? buf : j];
           if constexpr (CG == 1) ptx::mbar_arrive(bar);
-          else ptx::mbar_arrive_cluster(bar, 0);
+          else ptx::mbar_arrive_cluster(bar, (uint32_t)(pair * CG));   // this pair's MMA issuer
         }
       };
 
@@ -853,6 +903,7 @@ static int env_int(const char* name, int dflt) {
 struct Knobs {
   int cg = 2, nt = 0, group = GROUP_M, apol = -1, bpol = -1, cpol = -1, prefetch = 0, sched_static = 0;
   int epi_warps = 4;
+  int pairs = 1;
   int chain = 1;
   int cpf = 0;
   int stagger = 0;
@@ -871,6 +922,7 @@ static const Knobs& knobs() {
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
+    k.pairs = env_int("UM_GEMM_PAIRS", 1) == 2 ? 2 : 1;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
@@ -901,38 +953,50 @@ static std::atomic<int> g_grid_limit[64];
 
 static int grid_limit(int device) { return (device >= 0 && device < 64) ? g_grid_limit[device].load() : 0; }
 
-template <int CG, int NT, int EW, int GW>
+template <int CG, int NT, int EW, int GW, int NP = 1>
 static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   using C = Cfg<CG, NT, EW, GW>;
   const int total_tiles = args.total_tiles;
   static bool attr_set[64] = {false};
   if (device < 0 || device >= 64) return fail(UM_EVALUE, "device index out of range");
   if (!attr_set[device]) {
-    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT, EW, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UM_CUDA_CHECK(cudaFuncSetAttribute(gemm_bf16_kernel<CG, NT, EW, GW, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES));
     attr_set[device] = true;
   }
   int sms = 0;
   UM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  // the persistent grid, in CTA pairs (CG == 2) or CTAs: one per SM.  NP == 2
+  // asks for clusters of 4 (two pairs sharing B by multicast) where a GPC has
+  // room for them and falls back to plain pairs elsewhere (a GPC's SM count is
+  // not a multiple of 4: clusters of 4 alone would leave ~16 of 148 SMs idle);
+  // a lone pair runs the two halves of a 512-row tile in turn
+  int units = sms / CG;
+  const int tile_units = NP == 2 ? 2 * total_tiles : total_tiles;
   // with in-kernel gets every SM joins (its get warps pull even when it gets no tile)
-  int clusters = args.ngets > 0 ? sms / CG : std::min(total_tiles, sms / CG);
+  if (args.ngets == 0) units = std::min(units, tile_units);
   // co-resident ranks share the device: cap each launch's persistent grid so
   // their launches (and the pulls inside them) run side by side
   const int cap = grid_limit(device);
-  if (cap > 0) clusters = std::max(1, std::min(clusters, cap));
+  if (cap > 0) units = std::max(1, std::min(units, cap));
+  if (NP == 2) units = std::max(2, units & ~1);   // the grid must divide into clusters of 4
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.gridDim = dim3(units * CG, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributePreferredClusterDimension;
+  attr[1].val.preferredClusterDim.x = CG * NP;
+  attr[1].val.preferredClusterDim.y = 1;
+  attr[1].val.preferredClusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW, GW>, args));
+  cfg.numAttrs = NP == 2 ? 2 : 1;
+  UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW, GW, NP>, args));
   return UM_OK;
 }
 
@@ -1003,7 +1067,7 @@ struct StageCopy {
   size_t spitch, width, height;
 };
 struct Prepared {
-  int device = 0, CG = 2, NT = 256, EW = 4, ngets = 0, nslots = 0;
+  int device = 0, CG = 2, NT = 256, EW = 4, NP = 1, ngets = 0, nslots = 0;
   bool persistent = false, empty = true;
   void* scratch = nullptr;    // aligned copies of misaligned operand slices
   void* dbuf = nullptr;       // work list + tensor maps of > MAX_INLINE_OPS ops
@@ -1085,6 +1149,9 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   P->CG = CG;
   P->NT = NT;
   P->EW = (CG == 2 && kn.epi_warps == 8) ? 8 : 4;
+  // experimental: clusters of 2 pairs sharing B by TMA multicast (UM_GEMM_PAIRS=2)
+  P->NP = (CG == 2 && NT == 512 && P->EW == 4 && kn.pairs == 2) ? 2 : 1;
+  const int NPAIR = P->NP;
 
   std::vector<Work> works;
   std::vector<CUtensorMap> maps;
@@ -1110,7 +1177,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   }
   if ((int)slot_flags.size() > MAX_SLOTS)
     return fail(UM_EVALUE, "more than " + std::to_string(MAX_SLOTS) + " distinct done_flags in one launch");
-  const int epi_arrivals = (CG == 2 ? 2 : 1) * ((CG == 2 && kn.epi_warps == 8) ? 8 : 4);
+  const int epi_arrivals = (CG == 2 ? 2 : 1) * ((CG == 2 && kn.epi_warps == 8) ? 8 : 4) * NPAIR;
   for (int i = 0; i < nops; ++i) {
     const um_gemm_op& op = ops[i];
     if (op.c_remote && op.c.dtype == UM_F32 && (reinterpret_cast<uintptr_t>(op.c.base) & 3))
@@ -1134,7 +1201,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.m = (int32_t)m;
     w.n = (int32_t)n;
     w.k = (int32_t)k;
-    w.tiles_m = (int32_t)((m + BM * CG - 1) / (BM * CG));
+    w.tiles_m = (int32_t)((m + BM * CG * NPAIR - 1) / (BM * CG * NPAIR));
     w.tiles_n = (int32_t)((n + NT - 1) / NT);
     w.num_kb = (int32_t)((k + BK - 1) / BK);
     w.seg_kb = w.num_kb;
@@ -1162,6 +1229,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.wait_mask = op.get_mask;
     w.c_prefetch = kn.cpf;
     w.stagger = kn.stagger;
+    w.debug_halfb = env_int("UM_GEMM_DEBUG_HALFB", 0) ? 1 : 0;
     w.a_fine = op.a_get;
     w.b_fine = op.b_get;
     w.group = kn.group;
@@ -1340,6 +1408,8 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   int rc;
   const bool g = P->ngets > 0;
   if (P->CG == 1) rc = g ? launch<1, 256, 4, GET_WARPS>(args, P->device, stream) : launch<1, 256, 4, 0>(args, P->device, stream);
+  else if (P->NT == 512 && P->NP == 2)
+    rc = g ? launch<2, 512, 4, GET_WARPS, 2>(args, P->device, stream) : launch<2, 512, 4, 0, 2>(args, P->device, stream);
   else if (P->NT == 512 && P->EW == 8)
     rc = g ? launch<2, 512, 8, GET_WARPS>(args, P->device, stream) : launch<2, 512, 8, 0>(args, P->device, stream);
   else if (P->NT == 512)
@@ -1355,14 +1425,16 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
     cudaStreamSynchronize(stream);
     cudaFreeAsync(prof, stream);
     double tot = 0, full = 0, tmem = 0, tile = 0;
-    int n = 0;
+    int n = 0, n4 = 0;
     for (int c = 0; c < 512; ++c)
       if (h[4 * c]) {
-        tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += h[4 * c + 3]; ++n;
+        const unsigned long long t3 = h[4 * c + 3] & ((1ull << 56) - 1);
+        tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += t3; ++n;
+        n4 += (h[4 * c + 3] >> 56) == 4;
       }
     if (n)
-      fprintf(stderr, "[um_gemm stalls] %d clusters, MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
-                      "%.1f %%, for the next tile %.1f %% of %.0f cycles\n", n, 100 * full / tot, 100 * tmem / tot,
+      fprintf(stderr, "[um_gemm stalls] %d pairs (%d in clusters of 4), MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
+                      "%.1f %%, for the next tile %.1f %% of %.0f cycles\n", n, n4, 100 * full / tot, 100 * tmem / tot,
               100 * tile / tot, tot / n);
   }
   return rc;

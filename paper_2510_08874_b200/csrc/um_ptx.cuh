@@ -181,6 +181,11 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -209,6 +214,17 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+// 2-CTA + multicast: the box lands at the same smem offset in every CTA of
+// `mask`; each destination's completion goes to its pair's even (leader) CTA.
+__device__ __forceinline__ void tma_load_2d_cg2_mc(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
+                                                   int32_t c1, uint16_t mask, uint64_t policy) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
       : "memory");
 }
 // Warm L2 with a box ahead of its load (no smem, no completion tracking).
