@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   constexpr int EPI_WARPS = EW;
   // NP pairs per cluster (NP == 2: a cluster of 4 CTAs computes a 512 x NT
   // super-tile; the two pairs share the B k-panel through TMA multicast)
-  static_assert(NP == 1 || (NP == 2 && CG == 2), "B multicast needs CTA pairs");
+  static_assert(NP == 1 || ((NP == 2 || NP == 4) && CG == 2), "B multicast needs CTA pairs");
   constexpr int CS = CG * NP;   // cluster size
   // small op lists travel inside the kernel parameters (no per-launch device
   // allocation or host->device copy); larger ones in a global-memory block
@@ -250,24 +250,24 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  // NP == 2 launches with a preferred cluster of 4 and a regular one of 2: the
-  // hardware forms clusters of 4 where a GPC has room and pairs elsewhere, so
-  // the cluster size (cs) and the number of pairs in it (np) are runtime values
+  // NP > 1 launches with a preferred cluster of 2*NP CTAs and a regular one of
+  // 2: the hardware forms the big clusters where a GPC has room and pairs
+  // elsewhere, so the cluster size (cs) and its pair count (np) are runtime values
   const uint32_t crank = (CS > 1) ? ptx::cluster_ctarank() : 0u;   // rank in the cluster
-  const int cs = NP == 2 ? (int)ptx::cluster_nctarank() : CS;       // this cluster's size
+  const int cs = NP > 1 ? (int)ptx::cluster_nctarank() : CS;        // this cluster's size
   const int np = cs / CG;                                           // pairs in this cluster
   const uint32_t cta_rank = crank % CG;                             // rank in the CTA pair
   const int pair = (int)(crank / CG);
   const bool leader = cta_rank == 0;                                // pair leader (issues the MMAs)
   const bool cleader = crank == 0;                                  // cluster leader (takes tiles)
   const int TQ_CONSUMERS = (cs - 1) /*peer producers*/ + np /*MMA*/ + EPI_WARPS * cs;
-  // tile-queue entries: the tile index, or for NP == 2 (tile << 1 | half) where
-  // a lone pair runs the two 256-row halves of a 512-row tile one after the other
+  // tile-queue entries: the tile index, or for NP > 1 (tile * NP + part) where
+  // a lone pair runs the NP 256-row parts of a tile one after the other
   auto decode = [&](int q, int& t, int& row_off) {
     int sub = 0;
-    if constexpr (NP == 2) {
-      t = q >> 1;
-      sub = np == 2 ? pair : (q & 1);
+    if constexpr (NP > 1) {
+      t = q / NP;
+      sub = np == NP ? pair : (q % NP);
     } else {
       t = q;
     }
@@ -356,13 +356,13 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           // take the next tile and publish it to every CTA of the cluster
           const int slot = i % TQ;
           ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
-          if (NP == 2 && np == 1 && (i & 1)) {
-            q += 1;   // second half of the tile taken at i - 1
+          if (NP > 1 && np == 1 && (i % NP) != 0) {
+            q += 1;   // next part of the tile taken NP entries ago
           } else {
             int t = (NP == 1 && works[0].sched_static) ? (int)(blockIdx.x / CS) + i * (int)(gridDim.x / CS)  // A/B knob
                                                        : atomicAdd(tile_counter, 1);
             if (t > total_tiles) t = total_tiles;
-            q = NP == 2 ? t << 1 : t;
+            q = t * NP;
           }
           tq[slot] = q;
           if constexpr (CS > 1) {
@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           // (profiling only, UM_GEMM_DEBUG_HALFB: wrong results) skip the second
           // accumulator's B sub-tiles -> bound on what halving B traffic can buy
           const bool halfb = NP == 1 && C::NACC == 2 && works[0].debug_halfb;
-          const bool mcast = NP == 2 && np == 2;
+          constexpr uint32_t MC_MASK = NP == 4 ? 0x55u : 0x5u;   // pair rank 0 of every pair
+          const bool mcast = NP > 1 && np == NP;
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (halfb ? C::B_BYTES / 2 : 0)) * CG);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
           uint8_t* sb = smem_b + stage * C::B_BYTES;
@@ -462,11 +463,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               uint8_t* dst = sb + qsub * SUB_BYTES;
               const int col = bcol + j * UMMA_N + s * 64;
               if (mcast) {
-                // the CTA of the other pair with the same pair rank needs the same
-                // B sub-tiles: each loads half of them into both (multicast)
-                if ((qsub * 2) / C::B_SUBS != pair) continue;
-                ptx::tma_load_2d_cg2_mc(dst, mbm, &full[stage], col, krow,
-                                        (uint16_t)((1u << crank) | (1u << (crank ^ CG))), pb);
+                // the CTAs with this pair rank in the other pairs need the same B
+                // sub-tiles: each loads 1/NP of them into all (multicast)
+                if ((qsub * NP) / C::B_SUBS != pair) continue;
+                ptx::tma_load_2d_cg2_mc(dst, mbm, &full[stage], col, krow, (uint16_t)(MC_MASK << cta_rank), pb);
               } else if constexpr (CG == 1) {
                 ptx::tma_load_2d(dst, mbm, &full[stage], col, krow, pb);
               } else {
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     if (leader && lane == 0) {
       constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 1);
       // a stage is free once every pair sharing its B (multicast) has consumed it
-      const uint16_t EMPTY_MASK = np == 2 ? (uint16_t)0xF : (uint16_t)0x3;
+      const uint16_t EMPTY_MASK = (uint16_t)((1u << cs) - 1);
       const uint16_t PAIR_MASK = (uint16_t)(0x3u << (pair * CG));
       int stage = 0;
       uint32_t phase = 0;
@@ -922,7 +922,8 @@ static const Knobs& knobs() {
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
-    k.pairs = env_int("UM_GEMM_PAIRS", 1) == 2 ? 2 : 1;
+    k.pairs = env_int("UM_GEMM_PAIRS", 1);
+    if (k.pairs != 2 && k.pairs != 4) k.pairs = 1;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
@@ -972,14 +973,37 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   // not a multiple of 4: clusters of 4 alone would leave ~16 of 148 SMs idle);
   // a lone pair runs the two halves of a 512-row tile in turn
   int units = sms / CG;
-  const int tile_units = NP == 2 ? 2 * total_tiles : total_tiles;
+  const int tile_units = NP * total_tiles;
   // with in-kernel gets every SM joins (its get warps pull even when it gets no tile)
   if (args.ngets == 0) units = std::min(units, tile_units);
   // co-resident ranks share the device: cap each launch's persistent grid so
   // their launches (and the pulls inside them) run side by side
   const int cap = grid_limit(device);
   if (cap > 0) units = std::max(1, std::min(units, cap));
-  if (NP == 2) units = std::max(2, units & ~1);   // the grid must divide into clusters of 4
+  if (NP > 1) units = std::max(NP, units - units % NP);   // the grid must divide into big clusters
+  static int occ[64] = {0};
+  static const bool fixed = getenv("UM_GEMM_PAIRS_FIXED") && atoi(getenv("UM_GEMM_PAIRS_FIXED")) == 1;
+  if (NP > 1 && !occ[device]) {
+    // how many of the big clusters can be resident at once (A/B knob
+    // UM_GEMM_PAIRS_FIXED=1 launches only big clusters, sized by this)
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(units * CG, 1, 1);
+    q.blockDim = dim3(C::NUM_THREADS, 1, 1);
+    q.dynamicSmemBytes = C::SMEM_BYTES;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = CG * NP;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = -1;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<CG, NT, EW, GW, NP>, &q);
+    if (args.prof) fprintf(stderr, "[um_gemm stalls] max resident clusters of %d: %d (%s)\n", CG * NP, n, cudaGetErrorString(e));
+    cudaGetLastError();
+    occ[device] = (e == cudaSuccess && n > 0) ? n : 1;
+  }
+  if (NP > 1 && fixed) units = std::min(units, occ[device] * NP);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
@@ -987,7 +1011,7 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = (NP > 1 && fixed) ? CG * NP : CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributePreferredClusterDimension;
@@ -995,7 +1019,7 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   attr[1].val.preferredClusterDim.y = 1;
   attr[1].val.preferredClusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = NP == 2 ? 2 : 1;
+  cfg.numAttrs = (NP > 1 && !fixed) ? 2 : 1;
   UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW, GW, NP>, args));
   return UM_OK;
 }
@@ -1150,7 +1174,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   P->NT = NT;
   P->EW = (CG == 2 && kn.epi_warps == 8) ? 8 : 4;
   // experimental: clusters of 2 pairs sharing B by TMA multicast (UM_GEMM_PAIRS=2)
-  P->NP = (CG == 2 && NT == 512 && P->EW == 4 && kn.pairs == 2) ? 2 : 1;
+  P->NP = (CG == 2 && NT == 512 && P->EW == 4) ? kn.pairs : 1;
   const int NPAIR = P->NP;
 
   std::vector<Work> works;
@@ -1410,6 +1434,8 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   if (P->CG == 1) rc = g ? launch<1, 256, 4, GET_WARPS>(args, P->device, stream) : launch<1, 256, 4, 0>(args, P->device, stream);
   else if (P->NT == 512 && P->NP == 2)
     rc = g ? launch<2, 512, 4, GET_WARPS, 2>(args, P->device, stream) : launch<2, 512, 4, 0, 2>(args, P->device, stream);
+  else if (P->NT == 512 && P->NP == 4)
+    rc = g ? launch<2, 512, 4, GET_WARPS, 4>(args, P->device, stream) : launch<2, 512, 4, 0, 4>(args, P->device, stream);
   else if (P->NT == 512 && P->EW == 8)
     rc = g ? launch<2, 512, 8, GET_WARPS>(args, P->device, stream) : launch<2, 512, 8, 0>(args, P->device, stream);
   else if (P->NT == 512)
@@ -1430,10 +1456,10 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
       if (h[4 * c]) {
         const unsigned long long t3 = h[4 * c + 3] & ((1ull << 56) - 1);
         tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += t3; ++n;
-        n4 += (h[4 * c + 3] >> 56) == 4;
+        n4 += (h[4 * c + 3] >> 56) > 2;
       }
     if (n)
-      fprintf(stderr, "[um_gemm stalls] %d pairs (%d in clusters of 4), MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
+      fprintf(stderr, "[um_gemm stalls] %d pairs (%d in clusters > 2), MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
                       "%.1f %%, for the next tile %.1f %% of %.0f cycles\n", n, n4, 100 * full / tot, 100 * tmem / tot,
               100 * tile / tot, tot / n);
   }
