@@ -144,6 +144,10 @@ typedef struct {
                               those ops to *done_flag (release, system scope; may be a
                               peer / IPC-mapped word), so a consumer expecting n ops
                               waits for *done_flag >= n whatever the launch split  */
+  int32_t done_piece;      /* nonzero: this entry is a piece of an op that another entry
+                              sharing done_flag counts (not added); give the count to the
+                              piece issued last, so launches in stream order cover all  */
+  int32_t reserved;        /* zero */
 } um_gemm_op;
 
 /* A pull executed INSIDE the GEMM launch (um_gemm_acc_fused): src slice

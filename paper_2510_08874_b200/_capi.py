@@ -71,7 +71,8 @@ class UmGemmOp(ctypes.Structure):
     _fields_ = [("a", UmView), ("b", UmView), ("c", UmView),
                 ("c_remote", ctypes.c_int32), ("wait_value", ctypes.c_uint32),
                 ("wait_flag", ctypes.c_void_p), ("a_get", ctypes.c_int32), ("b_get", ctypes.c_int32),
-                ("get_mask", ctypes.c_uint64), ("done_flag", ctypes.c_void_p)]
+                ("get_mask", ctypes.c_uint64), ("done_flag", ctypes.c_void_p),
+                ("done_piece", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class UmGetDesc(ctypes.Structure):

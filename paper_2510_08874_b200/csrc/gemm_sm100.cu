@@ -1194,8 +1194,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
       if ((reinterpret_cast<uintptr_t>(f) & 3) != 0) return fail(UM_EVALUE, "done_flag must be 4-byte aligned");
       slot_flags.push_back(f);
       slot_expected.push_back(0);
-      slot_inc.push_back(1);
-    } else {
+      slot_inc.push_back(ops[i].done_piece ? 0 : 1);
+    } else if (!ops[i].done_piece) {
       ++slot_inc[it - slot_flags.begin()];
     }
   }

@@ -190,6 +190,7 @@ class _RankRun:
                 plan.actions.append(("wait", j))
                 waited[j] = True
 
+        last_piece = {(i, m0, m1): it for it, (i, _, m0, m1, *_) in enumerate(items)}
         for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
             op = s.ops[i]
             srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
@@ -243,6 +244,8 @@ class _RankRun:
             g.get_mask = sum(1 << gets_slot[u] for u in units if u in gets_slot and u not in fine.values())
             if self.signals is not None and i in self.signals:
                 g.done_flag = self.signals[i][1](m0, m1)
+                # pieces of one (op, sub-slice) along n: the last one issued counts
+                g.done_piece = 1 if it != last_piece[(i, m0, m1)] else 0
             batch.append(g)
             batch_remote += int(remote)
         flush()

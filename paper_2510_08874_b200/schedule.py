@@ -160,7 +160,9 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: di
     # A and B tiles) runs as sub-ops that each wait only for their part of
     # the pull.  Default split: along m when the pulled A dominates, along n
     # when B does (rows / columns of C: no extra C traffic, the tensor cores
-    # start once B / A and the first A / B band have landed).  k_split > 1
+    # start once B / A and the first A / B band have landed); along both
+    # when A and B are both pulled (each sub-op then waits for one A row band
+    # and one B column band, not for a whole operand).  k_split > 1
     # instead cuts k into slabs (every sub-op waits for one A and one B
     # slab, at the price of one more fp32 C read-modify-write per slab).
     first_user: dict = {}
@@ -184,10 +186,30 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: di
         nsub, dim = 1, None
         if row_cuts is not None and i in row_cuts:
             cuts_i = sorted({0, mlen} | {c for c in row_cuts[i] if 0 < c < mlen})
+            # a large pulled B is also cut along n, so the first sub-ops wait for
+            # one column band of it, not the whole tile (cfg4 at p = 8)
+            nc = [0, nlen]
+            if (not unfused_remote and cfg.k_split <= 1 and cfg.mn_split > 1 and pb >= _SPLIT_BYTES // 2
+                    and nlen >= 2 * _SPLIT_MIN):
+                sn = min(cfg.mn_split, nlen // _SPLIT_MIN)
+                nc = [nlen * t // sn // 64 * 64 for t in range(sn)] + [nlen]
             for t in range(len(cuts_i) - 1):
-                items.append((i, t, cuts_i[t], cuts_i[t + 1], 0, nlen, 0, klen))
+                for b_ in range(len(nc) - 1):
+                    items.append((i, t * (len(nc) - 1) + b_, cuts_i[t], cuts_i[t + 1], nc[b_], nc[b_ + 1], 0, klen))
             continue
         if not unfused_remote and pa + pb >= _SPLIT_BYTES:
+            if (cfg.k_split <= 1 and cfg.mn_split > 1 and min(pa, pb) >= _SPLIT_BYTES // 2
+                    and mlen >= 2 * _SPLIT_MIN and nlen >= 2 * _SPLIT_MIN):
+                # both operands pulled (cfg4 p=8: whole A and B tiles): a grid of
+                # sub-ops, each waiting for one A row band and one B column band,
+                # issued row by row so the first needs 1/mn_split of each pull
+                sm, sn = min(cfg.mn_split, mlen // _SPLIT_MIN), min(cfg.mn_split, nlen // _SPLIT_MIN)
+                mc = [mlen * t // sm // 64 * 64 for t in range(sm)] + [mlen]
+                nc = [nlen * t // sn // 64 * 64 for t in range(sn)] + [nlen]
+                for a_ in range(sm):
+                    for b_ in range(sn):
+                        items.append((i, a_ * sn + b_, mc[a_], mc[a_ + 1], nc[b_], nc[b_ + 1], 0, klen))
+                continue
             if cfg.k_split > 1 and klen >= 2 * _SPLIT_MIN:
                 nsub, dim = int(min(cfg.k_split, klen // _SPLIT_MIN, max(2, (pa + pb) // _SPLIT_BYTES))), "k"
             elif cfg.mn_split > 1 and pa >= pb and mlen >= 2 * _SPLIT_MIN:

@@ -38,7 +38,7 @@ def test_version_and_errors_without_gpu():
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_capi.UmView) == 8 + 5 * 8 + 2 * 4
     assert ctypes.sizeof(_capi.UmMatDesc) == 6 * 8 + 2 * 4
-    assert ctypes.sizeof(_capi.UmGemmOp) == 3 * ctypes.sizeof(_capi.UmView) + 40
+    assert ctypes.sizeof(_capi.UmGemmOp) == 3 * ctypes.sizeof(_capi.UmView) + 48
 
 
 def test_owner_rank_matches_python_tiling():

@@ -76,14 +76,31 @@ def test_cfg5_p8_b_tiles_banded_into_k_slabs():
         check_cover(sched, items, bands, need)
 
 
-def test_cfg4_p8_whole_tile_op_split_along_m():
+def test_cfg4_p8_whole_tile_op_split_into_a_grid():
     A, B, C = problem(16384, 16384, 16384, 8, "2d", "2d", "2d", 2, 2, 2)
     sched, items, bands, need = plan(A, B, C, 3)          # rank 3 pulls one A and one B tile (128 MiB each)
     assert len(sched.ops) == 1 and len(sched.fetches) == 2
-    assert [(m0, m1) for _, _, m0, m1, *_ in items] == [(0, 2048), (2048, 4096), (4096, 6144), (6144, 8192)]
+    # both operands pulled: 4 x 4 sub-ops, row by row; each waits for one A row
+    # band and one B column band (32 MiB each), the first for 1/4 of each pull
+    q = [(0, 2048), (2048, 4096), (4096, 6144), (6144, 8192)]
+    assert [(m0, m1, n0, n1) for _, _, m0, m1, n0, n1, _, _ in items] == [(*a, *b) for a in q for b in q]
     ja, jb = sched.a_src[0], sched.b_src[0]
-    assert len(bands[ja]) == 4 and len(bands[jb]) == 1
-    assert [need[(it, ja)] for it in range(4)] == [[0], [1], [2], [3]]
+    assert bands[ja] == [(r0, r1, 0, 8192) for r0, r1 in q] and bands[jb] == [(0, 8192, c0, c1) for c0, c1 in q]
+    assert [need[(it, ja)] for it in range(16)] == [[it // 4] for it in range(16)]
+    assert [need[(it, jb)] for it in range(16)] == [[it % 4] for it in range(16)]
+    check_cover(sched, items, bands, need)
+    # mn_split = 2: a 2 x 2 grid
+    sched, items, bands, need = plan(A, B, C, 3, mn_split=2)
+    assert len(items) == 4
+    check_cover(sched, items, bands, need)
+    # overlapped replica reduction: the op is cut at the reduction rows, and a
+    # large pulled B along n as well
+    cuts = [1024 * t for t in range(1, 8)]
+    cfg = ExecConfig()
+    items, bands, need = rt.plan_bands(sched, [True] * len(sched.fetches), cfg, {0: cuts})
+    assert len(items) == 8 * 4
+    assert [(m0, m1) for _, _, m0, m1, *_ in items[:5]] == [(0, 1024)] * 4 + [(1024, 2048)]
+    assert bands[jb] == [(0, 8192, c0, c1) for c0, c1 in q]
     check_cover(sched, items, bands, need)
     # k split instead: A banded by columns, B by rows, one slab each
     sched, items, bands, need = plan(A, B, C, 3, k_split=4)
