@@ -4,7 +4,8 @@ Each C tile is cut into c * panels row sub-slices on 256-row boundaries; the
 reducer of sub-slice k is the owner of replica k mod c; every rank's ops are
 split exactly at the sub-slice rows and signal the sub-slice's flag; the
 reducer waits for `expected` ops — which must equal the number of items that
-will signal it, or the reduction would start early or never."""
+will signal it (the pieces of one op along n count once), or the reduction
+would start early or never."""
 
 import pytest
 
@@ -45,7 +46,11 @@ def test_sub_slices_reducers_and_expected_signals(case, panels):
         sched = rt.lower_direct(A, B, C, cfg, r)
         sig = ovl.signals_for(sched)
         items, _, _ = rt.plan_bands(sched, [True] * len(sched.fetches), cfg, {i: c for i, (c, _) in sig.items()})
-        for (i, t_, m0, m1, n0, n1, k0, k1) in items:
+        # n-pieces of one (op, sub-slice) count once (um_gemm_op.done_piece)
+        last = {(i, m0, m1): it for it, (i, _, m0, m1, *_) in enumerate(items)}
+        for it, (i, t_, m0, m1, n0, n1, k0, k1) in enumerate(items):
+            if last[(i, m0, m1)] != it:
+                continue
             op = sched.ops[i]
             lo = op.c_local.rows.lo
             key = (op.c_tile, ovl.sub_slice_of(op.c_tile, lo + m0))
