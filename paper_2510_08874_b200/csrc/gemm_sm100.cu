@@ -1260,7 +1260,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     // L2 eviction hints default to normal: measured on the box, evict_last on
     // the group-reused operand + evict_first on the streamed one lowered the
     // sustained rate (1144 vs 1211 TFLOP/s at group 16); kept as knobs.
-    w.a_pol = kn.apol >= 0 ? kn.apol : 0;
+    w.a_pol = kn.apol >= 0 ? kn.apol : 0;   // auto: set below
     w.b_pol = kn.bpol >= 0 ? kn.bpol : 0;
     w.c_pol = kn.cpol >= 0 && kn.cpol <= 2 ? kn.cpol : -1;
     w.prefetch = kn.prefetch;
@@ -1325,6 +1325,22 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     works.swap(cw);
     maps.swap(cm);
     total = tot;
+  }
+  // default L2 policies for a launch that is ONE large work on an unshared
+  // device: A evict_first (each A panel is read by the 4 concurrent tiles of a
+  // raster group, then done), B evict_last (a group's B panels are reused over
+  // the whole m sweep).  cfg2: DRAM reads 8.25 -> 7.9 GB per launch, +2-3 % on
+  // cfg2 / 16384^3 / cfg3 shapes in power-capped runs.  Multi-op launches and
+  // ranks sharing a GPU keep evict_normal (A slices reused across ops: cfg5
+  // p=8 co-resident -3 % with the hints).
+  {
+    int heads = 0;
+    for (const Work& w : works) heads += w.nseg > 0;
+    const bool streaming = heads == 1 && grid_limit(device) == 0;
+    for (Work& w : works) {
+      if (kn.apol < 0 && streaming) w.a_pol = 1;
+      if (kn.bpol < 0 && streaming) w.b_pol = 2;
+    }
   }
   // completion-signal arrivals: every epilogue warp of both CTAs, once per tile of each work head
   for (const Work& w : works)
