@@ -905,6 +905,7 @@ struct Knobs {
   int epi_warps = 4;
   int pairs = 1;
   int chain = 1;
+  int chain_waves = 6;
   int cpf = 0;
   int stagger = 0;
 };
@@ -925,6 +926,7 @@ static const Knobs& knobs() {
     k.pairs = env_int("UM_GEMM_PAIRS", 1);
     if (k.pairs != 2 && k.pairs != 4) k.pairs = 1;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
+    k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
   });
@@ -1293,20 +1295,47 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
       return x.c_ptr == y.c_ptr && x.c_row0 == y.c_row0 && x.c_col0 == y.c_col0 && x.m == y.m && x.n == y.n &&
              x.c_pitch == y.c_pitch && x.c_remote == y.c_remote && x.slot == y.slot && x.c_pol == y.c_pol;
     };
-    std::vector<Work> cw;
-    std::vector<CUtensorMap> cm;
+    std::vector<std::vector<size_t>> groups;
     std::vector<char> used(works.size(), 0);
-    int tot = 0;
     for (size_t i = 0; i < works.size(); ++i) {
       if (used[i]) continue;
       std::vector<size_t> grp = {i};
+      used[i] = 1;
       for (size_t j = i + 1; j < works.size(); ++j)
-        if (!used[j] && same_c(works[i], works[j])) grp.push_back(j);
+        if (!used[j] && same_c(works[i], works[j])) {
+          grp.push_back(j);
+          used[j] = 1;
+        }
+      groups.push_back(grp);
+    }
+    // long chains make long tiles: too few of them leave the last wave of the
+    // persistent grid half empty (cfg5 p=8: 8 chains x 32 tiles of k = 16384
+    // on 74 pairs = 3.5 waves of 0.2 ms).  Cap the chain length so the launch
+    // has >= chain_waves x pairs tiles (sub-chains of one C region accumulate
+    // into it with the same reduce-add).
+    int max_len = 1;
+    for (const auto& g : groups) max_len = std::max(max_len, (int)g.size());
+    if (kn.chain_waves > 0) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      const long target = (long)kn.chain_waves * (sms / CG);
+      auto tiles_at = [&](int L) {
+        long t = 0;
+        for (const auto& g : groups)
+          t += (long)works[g[0]].tiles_m * works[g[0]].tiles_n * (((int)g.size() + L - 1) / L);
+        return t;
+      };
+      while (max_len > 1 && tiles_at(max_len) < target) max_len = (max_len + 1) / 2;
+    }
+    std::vector<Work> cw;
+    std::vector<CUtensorMap> cm;
+    int tot = 0;
+    for (const auto& grp_all : groups)
+      for (size_t s0 = 0; s0 < grp_all.size(); s0 += max_len) {
+      const std::vector<size_t> grp(grp_all.begin() + s0, grp_all.begin() + std::min(grp_all.size(), s0 + max_len));
+      const size_t i = grp[0];
       int kb = 0;
-      for (size_t g : grp) {
-        used[g] = 1;
-        kb += works[g].seg_kb;
-      }
+      for (size_t g : grp) kb += works[g].seg_kb;
       Work head = works[i];
       head.nseg = (int32_t)grp.size();
       head.num_kb = kb;
