@@ -469,9 +469,47 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     e1.record()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    # the e2e roofline: this box's pinned-memory copy bandwidth, each direction
+    # alone and both at once (PCIe is full duplex); floor = the slower direction
+    # of the concurrent pair
+    bw = pcie_bandwidth(dev)
+    floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "api": "hostio.multiply_from_host",
-            "panels": args.panels, "copy_streams": args.copy_streams}
+            "panels": args.panels, "copy_streams": args.copy_streams,
+            "roofline": {"bound": "pcie", "floor_ms_per_step": floor_ms, "frac": floor_ms / ms, **bw}}
+
+
+def pcie_bandwidth(dev, nbytes: int = 1 << 30, reps: int = 3) -> dict:
+    """Pinned host <-> device copy bandwidth (GB/s), one direction alone and both concurrently."""
+    import torch
+
+    h_src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_dst = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_src = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s_up, s_down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(streams_ops):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            evs = []
+            for st_, op in streams_ops:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(st_):
+                    e0.record()
+                    op()
+                    e1.record()
+                evs.append((e0, e1))
+            torch.cuda.synchronize(dev)
+            best = min(best, max(a.elapsed_time(b) for a, b in evs))
+        return nbytes / (best * 1e-3) / 1e9
+
+    up = (s_up, lambda: d_dst.copy_(h_src, non_blocking=True))
+    down = (s_down, lambda: h_dst.copy_(d_src, non_blocking=True))
+    both = timed([up, down])
+    return {"h2d_gbs": timed([up]), "d2h_gbs": timed([down]), "h2d_concurrent_gbs": both, "d2h_concurrent_gbs": both}
 
 
 def main():
