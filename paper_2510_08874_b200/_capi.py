@@ -17,7 +17,10 @@ from paper_2510_08874_b200.errors import ConfigError, ContractError, OwnershipEr
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # UNIMUL_B200_LIB points at an alternative build of the same library (A/B
 # experiments with compile-time variants); the default is the in-tree build.
-LIB_PATH = os.environ.get("UNIMUL_B200_LIB") or os.path.join(_HERE, "_lib", "libunimul_b200.so")
+# UM_GEMM_STALLS=1 needs the profiling build (`make -C paper_2510_08874_b200/csrc
+# prof`): the default library has no profiling code in its kernels.
+LIB_PATH = os.environ.get("UNIMUL_B200_LIB") or os.path.join(
+    _HERE, "_lib", "libunimul_b200_prof.so" if os.environ.get("UM_GEMM_STALLS") == "1" else "libunimul_b200.so")
 
 UM_OK = 0
 UM_ECONFIG = 1
@@ -132,7 +135,7 @@ def load():
         raise ImportError(
             f"unimul_b200 native library not built: {LIB_PATH} is missing. "
             "Run `python -c 'import __graft_entry__ as g; g.build()'` "
-            "or `make -C paper_2510_08874_b200/csrc`.")
+            "or `make -C paper_2510_08874_b200/csrc` (`make ... prof` for the UM_GEMM_STALLS build).")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)

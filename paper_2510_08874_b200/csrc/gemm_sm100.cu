@@ -189,6 +189,14 @@ constexpr int MAX_GETS = UM_GEMM_MAX_GETS;
 constexpr int GET_CHUNK_BYTES = 32 * 1024;
 constexpr int MAX_SLOTS = UM_GEMM_MAX_SIGNALS;
 constexpr int MAX_CHUNK_FLAGS = 1 << 16;  // per-chunk landed flags (fine-grained waits)
+// UM_PROFILE=1 (the separate libunimul_b200_prof.so, `make prof`) compiles in
+// the MMA-thread wait accounting and the block-0 timeline behind UM_GEMM_STALLS.
+// The default library has none of it: even untaken checks in the MMA issuer's
+// loop cost ~10 % on mid-size launches (measured, 4096^3).
+#ifndef UM_PROFILE
+#define UM_PROFILE 0
+#endif
+constexpr int TRACE_OFF = 4 * 512 - 16;   // profiling timeline stamps inside the prof buffer
 constexpr int CHUNK_FLAGS_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
 
 // Completion signal: once every tile of every op naming this slot has been
@@ -274,6 +282,16 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     row_off = sub * BM * CG + (int)cta_rank * BM;   // this CTA's rows in the tile
   };
 
+  // profiling (UM_GEMM_STALLS): block 0 stamps the globaltimer at milestones of
+  // its first tile, to see where a small launch's fixed latency goes
+  auto stamp = [&](int i) {
+#if UM_PROFILE
+    if (args.prof && blockIdx.x == 0) args.prof[TRACE_OFF + i] = ptx::globaltimer();
+#else
+    (void)i;
+#endif
+  };
+  if (threadIdx.x == 0) stamp(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -302,10 +320,14 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     for (int s = 0; s < args.nslots; ++s)   // a slot whose ops have no tile is complete at once
       if (args.slots[s].expected == 0) ptx::red_release_sys_add_u32(args.slots[s].flag, args.slots[s].increment);
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+  // warm the descriptors of the first works while the CTA sets up (the first
+  // TMA otherwise waits for its tensor map: ~1 us of a small launch)
+  if (warp == 0 && lane < 3 * 8 && lane / 3 < nwork) ptx::prefetch_tmap(&maps[lane]);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     // ===================== TMA producer (one thread per CTA) =====================
@@ -376,6 +398,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
         int t, row_off;
         decode(q, t, row_off);
+        if (i == 0) stamp(2);
         if (t >= total_tiles) {
           if (leader) {
             // this pair is done with the counter (its cluster leader took its
@@ -473,6 +496,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
                 ptx::tma_load_2d_cg2(dst, mbm, &full[stage], col, krow, pb);
               }
             }
+          if (i == 0 && kb == 0) stamp(3);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         }  // k-chain segments
@@ -491,6 +515,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       unsigned long long c_full = 0, c_tmem = 0, c_tile = 0;
       const unsigned long long c_begin = clock64();
       auto timed = [&](unsigned long long& acc, auto&& fn) {
+#if UM_PROFILE
         if (args.prof) {
           const unsigned long long t0 = clock64();
           fn();
@@ -498,6 +523,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         } else {
           fn();
         }
+#else
+        (void)acc;
+        fn();
+#endif
       };
       // all MMAs of one k-block into accumulator `acc_col`
       auto issue = [&](int stg, uint32_t acc_col, int j, bool first_kb) {
@@ -527,6 +556,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           ptx::tc_fence_after();
           for (int kb = 0; kb < num_kb; ++kb) {
             timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
+            if (it == 0 && kb == 0) stamp(4);
             ptx::tc_fence_after();
             issue(stage, buf * UMMA_N, 0, kb == 0);
             ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
@@ -582,6 +612,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           ptx::umma_commit<CG>(&tmem_full[1], PAIR_MASK);
         }
         if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], PAIR_MASK);
+        if (it == 0) stamp(5);
       }
       if (args.prof) {
         unsigned long long* o = args.prof + 4 * (blockIdx.x / CG);
@@ -711,6 +742,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       for (int j = 0; j < C::NACC; ++j) {
         // NACC == 1: one barrier per TMEM buffer; NACC == 2: one per accumulator
         ptx::mbar_wait(&tmem_full[C::NACC == 1 ? buf : j], tph);
+        if (it == 0 && j == 0 && e == 0 && lane == 0) stamp(6);
         ptx::tc_fence_after();
         const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * UMMA_N;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
@@ -735,6 +767,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           }
         }
       }
+      if (it == 0 && e == 0 && lane == 0) stamp(7);
       if (wk.slot >= 0) {
         // this warp's share of the tile is in C: complete its bulk writes, then
         // count it; the last arrival of the slot publishes the signal
@@ -752,6 +785,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();
+    if (e == 0 && lane == 0) stamp(8);
   } else if (args.ngets > 0) {
     // ===================== get engine (GET_WARPS warps per CTA) =====================
     // Pulls the launch's remote operand slices into local staging buffers while
@@ -831,11 +865,13 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     }
   }
 
+  if (threadIdx.x == 0) stamp(9);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+    if (lane == 0) stamp(10);
   }
 }
 
@@ -1497,12 +1533,22 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
     cudaFreeAsync(prof, stream);
     double tot = 0, full = 0, tmem = 0, tile = 0;
     int n = 0, n4 = 0;
-    for (int c = 0; c < 512; ++c)
+    for (int c = 0; c < TRACE_OFF / 4; ++c)
       if (h[4 * c]) {
         const unsigned long long t3 = h[4 * c + 3] & ((1ull << 56) - 1);
         tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += t3; ++n;
         n4 += (h[4 * c + 3] >> 56) > 2;
       }
+    if (h[TRACE_OFF]) {
+      fprintf(stderr, "[um_gemm stalls] block 0 timeline (us after entry): setup %.2f, first tile %.2f, first loads "
+                      "issued %.2f, first operands landed %.2f, first tile's MMAs committed %.2f, epilogue got TMEM "
+                      "%.2f, epilogue issued C %.2f, C writes complete %.2f, loops done %.2f, exit %.2f\n",
+              (h[TRACE_OFF + 1] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 2] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 3] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 4] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 5] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 6] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 7] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 8] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 9] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 10] - h[TRACE_OFF]) * 1e-3);
+    }
     if (n)
       fprintf(stderr, "[um_gemm stalls] %d pairs (%d in clusters > 2), MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "
                       "%.1f %%, for the next tile %.1f %% of %.0f cycles\n", n, n4, 100 * full / tot, 100 * tmem / tot,
