@@ -1271,12 +1271,15 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.tile_start = total;
     w.c_remote = op.c_remote;
     if (!op.c_remote) {
-      // profiling knob: UM_GEMM_EPI_DEBUG=store|none replaces the reduce-add
       static const char* dbg = getenv("UM_GEMM_EPI_DEBUG");
+      if (dbg && !strcmp(dbg, "red")) w.c_remote = 1;  // A/B: coalesced red.global epilogue for local C
+#if UM_PROFILE
+      // profiling build only (results not C += A.B): store|none replace the
+      // reduce-add, rmw assumes an exclusive writer of each C tile
       if (dbg && !strcmp(dbg, "store")) w.c_remote = 2;
       if (dbg && !strcmp(dbg, "none")) w.c_remote = 3;
-      if (dbg && !strcmp(dbg, "red")) w.c_remote = 1;  // coalesced red.global epilogue for local C
-      if (dbg && !strcmp(dbg, "rmw")) w.c_remote = 4;  // exclusive-writer load/add/store epilogue
+      if (dbg && !strcmp(dbg, "rmw")) w.c_remote = 4;
+#endif
     }
     w.a_row0 = (int32_t)op.a.row_lo;
     w.a_col0 = (int32_t)op.a.col_lo;
@@ -1291,7 +1294,11 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.wait_mask = op.get_mask;
     w.c_prefetch = kn.cpf;
     w.stagger = kn.stagger;
-    w.debug_halfb = env_int("UM_GEMM_DEBUG_HALFB", 0) ? 1 : 0;
+#if UM_PROFILE
+    w.debug_halfb = env_int("UM_GEMM_DEBUG_HALFB", 0) ? 1 : 0;   // profiling build only: wrong results
+#else
+    w.debug_halfb = 0;
+#endif
     w.a_fine = op.a_get;
     w.b_fine = op.b_get;
     w.group = kn.group;
