@@ -1,0 +1,64 @@
+"""K1 compile-time / launch-time variants selected by library knobs give the
+same exact results as the default (integer inputs, C += A.B).
+
+Each variant runs in a subprocess (the knobs are read once per process):
+one large single op (NT=512 pair tiles, L2 hints), a ragged op, and a batch
+of k-chunk ops sharing one C region (k-chains, capped by UM_GEMM_CHAIN_WAVES).
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import ctypes, sys, torch
+sys.path.insert(0, '.')
+from paper_2510_08874_b200 import _capi as C, kernels
+lib = C.load()
+g = torch.Generator(device='cuda').manual_seed(11)
+def ints(r, c):
+    return torch.randint(-8, 9, (r, c), generator=g, device='cuda').to(torch.bfloat16)
+def view(t, r0, r1, c0, c1, dt):
+    return C.UmView(t.data_ptr(), r0, r1, c0, c1, t.stride(0), dt, 0)
+for m, n, k in ((8192, 4096, 512), (1000, 1000, 1000)):
+    a, b = ints(m, k), ints(k, n)
+    c = torch.randint(-8, 9, (m, n), generator=g, device='cuda').float()
+    ref = c.double() + a.double() @ b.double()
+    kernels.gemm_accumulate(a, b, c)
+    assert torch.equal(c.double(), ref), (m, n, k)
+# 8 ops accumulating k-chunks of one product into the same C (one launch)
+m, n, k, parts = 2048, 2048, 4096, 8
+a, b = ints(m, k), ints(k, n)
+c = torch.zeros(m, n, device='cuda')
+kc = k // parts
+ops = (C.UmGemmOp * parts)(*[C.UmGemmOp(view(a, 0, m, i * kc, (i + 1) * kc, C.UM_BF16),
+                                        view(b, i * kc, (i + 1) * kc, 0, n, C.UM_BF16),
+                                        view(c, 0, m, 0, n, C.UM_F32), 0) for i in range(parts)])
+C.check(lib.um_gemm_acc_batch(ops, parts, 0, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), 'batch')
+torch.cuda.synchronize()
+assert torch.equal(c.double(), a.double() @ b.double())
+print('OK')
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {},
+    {"UM_GEMM_PAIRS": "2"},                              # clusters of 2 pairs, B multicast (preferred 4)
+    {"UM_GEMM_PAIRS": "4"},                              # preferred clusters of 8
+    {"UM_GEMM_PAIRS": "4", "UM_GEMM_PAIRS_FIXED": "1"},  # clusters of 8 only
+    {"UM_GEMM_NT": "256"},
+    {"UM_GEMM_EPI_WARPS": "8"},
+    {"UM_GEMM_CHAIN_WAVES": "0"},                        # uncapped k-chains
+    {"UM_GEMM_CHAIN": "0"},
+    {"UM_GEMM_EPI_DEBUG": "red"},                        # red.global epilogue for local C
+    {"UM_GEMM_APOL": "0", "UM_GEMM_BPOL": "0", "UM_GEMM_CPOL": "1"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_variant_exact(env):
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env), cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "OK" in out.stdout, (out.stdout[-1000:], out.stderr[-2000:])
