@@ -25,6 +25,18 @@ def test_library_exports_every_declared_symbol():
         assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
 
 
+def test_profiling_build_exports_the_same_api():
+    """`make prof` (UM_GEMM_STALLS) builds the same C-ABI with profiling compiled in."""
+    import pytest
+
+    prof = os.path.join(os.path.dirname(_capi.LIB_PATH), "libunimul_b200_prof.so")
+    if not os.path.exists(prof):
+        pytest.skip("profiling build not present (make -C paper_2510_08874_b200/csrc prof)")
+    lib = ctypes.CDLL(prof)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
 def test_version_and_errors_without_gpu():
     lib = _capi.load()
     assert b"sm_100a" in lib.um_version()
