@@ -30,8 +30,13 @@ from paper_2510_08874_b200.errors import ContractError
 class CapturedMultiply:
     """C += A @ B as a replayable CUDA graph (same semantics as execute_multiply)."""
 
-    def __init__(self, A, B, C, cfg: rt.ExecConfig | None = None, warmup: int = 1):
+    def __init__(self, A, B, C, cfg: rt.ExecConfig | None = None, warmup: int = 1, execution: str = "direct",
+                 machine=None, max_compute: int | None = None, max_comm: int | None = None):
+        """execution / machine / max_compute / max_comm as for execute_multiply: an
+        IR schedule ("ir:greedy", "ir:cost", "ir:exhaustive") is lowered once by
+        the warm-up multiplies and its replay captured like the direct path."""
         cfg = dataclasses.replace(cfg or rt.ExecConfig(), overlap_reduce=False)
+        run = dict(execution=execution, machine=machine, max_compute=max_compute, max_comm=max_comm)
         fab = A.fabric
         if fab.world.size != 1:
             raise ContractError("CapturedMultiply is single-process (multi-process runs need host barriers)")
@@ -40,7 +45,7 @@ class CapturedMultiply:
         # scheduler counters, so nothing is allocated while capturing (they are
         # real multiplies: C += A @ B each, counted like any other)
         for _ in range(max(1, warmup)):
-            rt.execute_multiply(A, B, C, cfg)
+            rt.execute_multiply(A, B, C, cfg, **run)
         torch.cuda.synchronize()
         before = fab.counters.__class__(fab.counters.nprocs)
         before.merge(fab.counters)
@@ -50,7 +55,7 @@ class CapturedMultiply:
         side.wait_stream(torch.cuda.current_stream())
         try:
             with torch.cuda.graph(self.graph, stream=side):
-                self.stats = rt.execute_multiply(A, B, C, cfg)
+                self.stats = rt.execute_multiply(A, B, C, cfg, **run)
         finally:
             eng.TRACE_ENABLED = trace
         # the capture ran the host-side counting of one multiply but executed
