@@ -197,6 +197,13 @@ constexpr int MAX_CHUNK_FLAGS = 1 << 16;  // per-chunk landed flags (fine-graine
 #define UM_PROFILE 0
 #endif
 constexpr int TRACE_OFF = 4 * 512 - 16;   // profiling timeline stamps inside the prof buffer
+// UM_GEMM_TIMELINE=<csv> (profiling build): per-pair tile spans and per-chunk
+// landing times of the in-kernel pulls, after the stall counters
+constexpr int TL_TILES = 96;                          // tiles recorded per pair
+constexpr int TL_OFF = 4 * 512;                       // [pair][tile][3] = tile, start, end (ns)
+constexpr int TL_CHUNKS = 32768;                      // chunk landing times recorded
+constexpr int TL_CHUNK_OFF = TL_OFF + 128 * TL_TILES * 3;
+constexpr int PROF_WORDS = TL_CHUNK_OFF + TL_CHUNKS;
 constexpr int CHUNK_FLAGS_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
 
 // Completion signal: once every tile of every op naming this slot has been
@@ -547,6 +554,14 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         timed(c_tile, [&] { t = next_tile(it); });
         decode(t, t, row_off_unused);
         if (t >= total_tiles) break;
+#if UM_PROFILE
+        const int tl_pair = (int)(blockIdx.x / CG);
+        if (args.prof && it < TL_TILES && tl_pair < 128) {
+          unsigned long long* e = args.prof + TL_OFF + (tl_pair * TL_TILES + it) * 3;
+          e[0] = (unsigned long long)t + 1;
+          e[1] = ptx::globaltimer();
+        }
+#endif
         const int w = find_work(works, nwork, t);
         const int num_kb = works[w].num_kb;
         const int buf = it % C::NBUF;
@@ -613,6 +628,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
         if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], PAIR_MASK);
         if (it == 0) stamp(5);
+#if UM_PROFILE
+        if (args.prof && it < TL_TILES && tl_pair < 128)   // all MMAs of the tile issued
+          args.prof[TL_OFF + (tl_pair * TL_TILES + it) * 3 + 2] = ptx::globaltimer();
+#endif
       }
       if (args.prof) {
         unsigned long long* o = args.prof + 4 * (blockIdx.x / CG);
@@ -860,6 +879,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       if (lane == 0) {
         __threadfence();
         atomicAdd(&done[j], 1);
+#if UM_PROFILE
+        if (args.prof && c < TL_CHUNKS) args.prof[TL_CHUNK_OFF + c] = ptx::globaltimer();
+#endif
         if (c < MAX_CHUNK_FLAGS) ptx::st_release_gpu_s32(&args.counters[CHUNK_FLAGS_OFF + c], 1);
       }
     }
@@ -1513,8 +1535,8 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   static const bool stalls = env_int("UM_GEMM_STALLS", 0) != 0;
   unsigned long long* prof = nullptr;
   if (stalls) {
-    UM_CUDA_CHECK(cudaMallocAsync(&prof, 4 * 512 * sizeof(unsigned long long), stream));
-    UM_CUDA_CHECK(cudaMemsetAsync(prof, 0, 4 * 512 * sizeof(unsigned long long), stream));
+    UM_CUDA_CHECK(cudaMallocAsync(&prof, PROF_WORDS * sizeof(unsigned long long), stream));
+    UM_CUDA_CHECK(cudaMemsetAsync(prof, 0, PROF_WORDS * sizeof(unsigned long long), stream));
   }
   args.prof = prof;
   int rc;
@@ -1534,7 +1556,7 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
     rc = g ? launch<2, 256, 4, GET_WARPS>(args, P->device, stream) : launch<2, 256, 4, 0>(args, P->device, stream);
   args.prof = nullptr;
   if (prof) {
-    std::vector<unsigned long long> h(4 * 512);
+    std::vector<unsigned long long> h(PROF_WORDS);
     cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     cudaFreeAsync(prof, stream);
@@ -1546,6 +1568,31 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
         tot += h[4 * c]; full += h[4 * c + 1]; tmem += h[4 * c + 2]; tile += t3; ++n;
         n4 += (h[4 * c + 3] >> 56) > 2;
       }
+    if (const char* tl = getenv("UM_GEMM_TIMELINE")) {
+      // append this launch's tile spans and chunk landings, ns after its first event
+      static int launch_no = 0;
+      unsigned long long t0 = ~0ull;
+      for (int i = 0; i < 128 * TL_TILES; ++i)
+        if (h[TL_OFF + 3 * i]) t0 = std::min(t0, h[TL_OFF + 3 * i + 1]);
+      for (int c = 0; c < TL_CHUNKS; ++c)
+        if (h[TL_CHUNK_OFF + c]) t0 = std::min(t0, h[TL_CHUNK_OFF + c]);
+      if (FILE* f = fopen(tl, launch_no == 0 ? "w" : "a")) {
+        if (launch_no == 0) fprintf(f, "launch,kind,pair,index,id,start_ns,end_ns\n");
+        for (int pr = 0; pr < 128; ++pr)
+          for (int i = 0; i < TL_TILES; ++i) {
+            const unsigned long long* e = &h[TL_OFF + (pr * TL_TILES + i) * 3];
+            if (e[0])
+              fprintf(f, "%d,tile,%d,%d,%llu,%llu,%llu\n", launch_no, pr, i, e[0] - 1, e[1] - t0,
+                      e[2] ? e[2] - t0 : 0ull);
+          }
+        for (int c = 0; c < TL_CHUNKS; ++c)
+          if (h[TL_CHUNK_OFF + c])
+            fprintf(f, "%d,chunk,-1,%d,%d,%llu,%llu\n", launch_no, c, c, h[TL_CHUNK_OFF + c] - t0,
+                    h[TL_CHUNK_OFF + c] - t0);
+        fclose(f);
+      }
+      ++launch_no;
+    }
     if (h[TRACE_OFF]) {
       fprintf(stderr, "[um_gemm stalls] block 0 timeline (us after entry): setup %.2f, first tile %.2f, first loads "
                       "issued %.2f, first operands landed %.2f, first tile's MMAs committed %.2f, epilogue got TMEM "
