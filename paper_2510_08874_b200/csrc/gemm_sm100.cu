@@ -964,6 +964,7 @@ struct Knobs {
   int pairs = 1;
   int chain = 1;
   int chain_waves = 6;
+  int tail_split = 0;
   int cpf = 0;
   int stagger = 0;
 };
@@ -985,6 +986,7 @@ static const Knobs& knobs() {
     if (k.pairs != 2 && k.pairs != 4) k.pairs = 1;
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
+    k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
   });
@@ -1414,6 +1416,57 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
         c.tile_start = tot;       // continuation: never the target of a tile index
         cw.push_back(c);
         for (int q = 0; q < 3; ++q) cm.push_back(maps[3 * grp[g] + q]);
+      }
+    }
+    works.swap(cw);
+    maps.swap(cm);
+    total = tot;
+  }
+  // the last wave of a fused launch (whose tail waits for the last pull) runs
+  // on short tiles: works issued last, about one wave of tiles, are split
+  // along k -- a chain into its segments, a single op into the two halves of
+  // its k range.  Every piece reduce-adds into C (an atomic C +=), so the
+  // pieces need no ordering among themselves.
+  if (ngets > 0 && kn.tail_split && !works.empty()) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const long wave = sms / CG;
+    std::vector<char> split(works.size(), 0);
+    long tail = 0;
+    for (size_t i = works.size(); i-- > 0 && tail < wave;) {
+      const Work& w = works[i];
+      if (w.nseg == 0) continue;                       // continuation: handled with its head
+      tail += (long)w.tiles_m * w.tiles_n;
+      split[i] = w.nseg > 1 ? 2 : (w.num_kb >= 8 ? 1 : 0);
+    }
+    std::vector<Work> cw;
+    std::vector<CUtensorMap> cm;
+    int tot = 0;
+    bool unchain = false;                              // inside a chain being split into its segments
+    auto emit = [&](Work x, size_t src, bool head) {
+      x.tile_start = tot;                              // continuation: the next head's start, never a target
+      if (head) tot += x.tiles_m * x.tiles_n;
+      cw.push_back(x);
+      for (int q = 0; q < 3; ++q) cm.push_back(maps[3 * src + q]);
+    };
+    for (size_t i = 0; i < works.size(); ++i) {
+      Work w = works[i];
+      if (w.nseg > 0) unchain = split[i] == 2;
+      if (split[i] == 1) {
+        const int h = w.num_kb / 2;
+        Work a = w, b = w;
+        a.num_kb = a.seg_kb = h;
+        b.num_kb = b.seg_kb = w.num_kb - h;
+        b.a_col0 += h * BK;
+        b.b_row0 += h * BK;
+        emit(a, i, true);
+        emit(b, i, true);
+      } else if (unchain) {
+        w.nseg = 1;                                    // every segment of the chain becomes a work
+        w.num_kb = w.seg_kb;
+        emit(w, i, true);
+      } else {
+        emit(w, i, w.nseg > 0);
       }
     }
     works.swap(cw);

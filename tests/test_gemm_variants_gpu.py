@@ -56,6 +56,7 @@ print('OK')
     {"UM_GEMM_CHAIN": "0"},
     {"UM_GEMM_EPI_DEBUG": "red"},                        # red.global epilogue for local C
     {"UM_GEMM_APOL": "0", "UM_GEMM_BPOL": "0", "UM_GEMM_CPOL": "1"},
+    {"UM_GEMM_TAIL_SPLIT": "1"},                         # last wave split along k (fused launches)
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_variant_exact(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
