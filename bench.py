@@ -4,10 +4,19 @@
 
 One step = one full `execute_multiply` (every get, GEMM, remote accumulate and
 replica reduction of the configuration) over synthetic operands resident in
-HBM.  N=1 runs BASELINE configs[1] (cfg2: 1D row-block A and C, B replicated,
-m=65536, n=k=8192) as its single-GPU instance (p = 1 rank); under torchrun
-(N>1) every process hosts one logical rank (p = N) of the same global
-problem, so total work is fixed ("strong" scaling).
+HBM.  The default workload is BASELINE configs[4] (cfg5: mismatched A 2D /
+B col / C row partitionings, 16384^3), the north-star size whose multi-GPU
+runs carry real one-sided traffic (496 MiB of pulls per rank at p=8); at
+N=1 it is one rank (p = 1).  `--config cfg2` etc. select the other BASELINE
+configurations.
+
+Multi-GPU: one process per GPU, each hosting one logical rank (p = N) of the
+same global problem, so total work is fixed ("strong" scaling).  Under
+torchrun the ranks come from the environment; `python bench.py --gpus N`
+without torchrun re-launches itself under `torch.distributed.run` with N
+processes.  Fewer visible GPUs than ranks is an error unless
+`--oversubscribe` (several ranks time-sharing a GPU: a functional test, not
+a measurement; n_gpus then counts the physical GPUs used).
 
 Printed JSON keys follow the driver contract; `value` is device-timed
 (CUDA events, max over ranks), `e2e` repeats the metric through the public
@@ -145,17 +154,49 @@ class ClockSampler:
 
 
 def k1_traffic(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the K1 launch from the committed
-    `ncu --set full` capture (profiles/r1_ncu_summary.json), or None if not captured
-    for this workload."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_summary.json")) as f:
-            prof = json.load(f)
+    """dram__bytes_read.sum + dram__bytes_write.sum of the K1 launch of this
+    workload from the newest committed `ncu --set full` capture
+    (profiles/*_ncu_summary.json, key k1_bench_<config>), labelled with the
+    capture's file, git SHA of the kernel build and date — ncu cannot run
+    inside the timed bench, so the figure is from a separate capture of the
+    same command, not from this run.  None if no capture exists."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                prof = json.load(f)
+        except Exception:  # noqa: BLE001
+            continue
         e = prof.get(f"k1_bench_{config}")
-        return None if e is None else {"bytes_per_launch": e["dram_bytes_per_launch"],
-                                       "source": "profiles/r1_ncu_summary.json:k1_bench_" + config}
-    except Exception:  # noqa: BLE001
-        return None
+        if e is not None:
+            return {"bytes_per_launch": e["dram_bytes_per_launch"],
+                    "source": f"profiles/{os.path.basename(path)}:k1_bench_{config}",
+                    "captured": {k: e.get(k) for k in ("git_sha", "date", "command") if k in e} or "round-1 build"}
+    return None
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-launch this script as N ranks (one process
+    per GPU) under torch.distributed.run; refuse when fewer GPUs are visible."""
+    import torch
+
+    ndev = torch.cuda.device_count()
+    if ndev < args.gpus and not args.oversubscribe:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {ndev} CUDA device(s) visible "
+                                                     f"(pass --oversubscribe to time-share GPUs)"}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def blas_threads(n: int):
@@ -326,7 +367,12 @@ def b200_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ndev = torch.cuda.device_count()
-    local = local % ndev          # several ranks may share a GPU (e.g. 2 ranks on a 1-GPU box)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
+    if world > ndev and not args.oversubscribe:
+        raise SystemExit(f"bench.py: {world} ranks but {ndev} visible GPU(s); --oversubscribe to time-share")
+    n_gpus = min(world, ndev)     # physical GPUs in use (ranks share a GPU only under --oversubscribe)
+    local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
         if world <= ndev:
@@ -411,7 +457,7 @@ def b200_arm(args):
     # A read once, B read once, C read + written once (fp32 C += A.B), per K1 launch
     algo_bytes = (2 * m * k + 2 * k * n + 8 * m * n) / p
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                "config": {"workload": f"{args.config}: {desc}", "m": m, "n": n, "k": k, "p": p,
@@ -419,11 +465,13 @@ def b200_arm(args):
                           "inputs": "bf16 uniform(-1,1) generated on device (K5), C fp32",
                           "l2": "inputs larger than L2 (A %.0f MiB, C %.0f MiB per rank > 126 MB)" % (
                               m * k * 2 / p / 2**20, m * n * 4 / p / 2**20)},
-               "frac_of_peak": value / (world * peak), "peak_per_gpu_tflops": peak, "peak_kind": peak_kind,
+               "frac_of_peak": value / (n_gpus * peak), "peak_per_gpu_tflops": peak, "peak_kind": peak_kind,
+               "ranks": world, "oversubscribed": world > n_gpus,
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": (achieved / peak) if achieved else None,
                             "traffic": (traffic or {}).get("bytes_per_launch"),
                             "traffic_source": (traffic or {}).get("source"),
+                            "traffic_captured": (traffic or {}).get("captured"),
                             "algorithmic_bytes_per_launch": algo_bytes,
                             "kernel": "um::gemm::gemm_bf16_kernel<2>", "launches_timed": len(durs),
                             "algorithmic_flops_per_launch": (sum(kflops) / len(kflops)) if kflops else None},
@@ -518,7 +566,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="allow more ranks than visible GPUs (ranks time-share a GPU; functional runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--panels", type=int, default=32, help="row panels of the host-streaming e2e path")
     ap.add_argument("--copy-streams", type=int, default=1, help="copy streams per direction in the e2e path (measured: 1 best)")
@@ -530,6 +580,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         b200_arm(args)
 

@@ -1666,6 +1666,25 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
 
 int launch_batch(const um_gemm_op* ops, int nops, const um_get_desc* gets, int ngets, int device,
                  cudaStream_t stream) {
+  // A one-shot launch keeps its work list in the kernel's parameter block: a
+  // longer op list without in-kernel gets runs as consecutive launches of at
+  // most MAX_INLINE_OPS ops (stream order keeps C += exact).  The descriptor
+  // block of a longer list would otherwise be a device buffer filled from a
+  // stack-local host vector, which a CUDA-graph capture cannot record safely.
+  if (nops > MAX_INLINE_OPS && ngets == 0) {
+    for (int i = 0; i < nops; i += MAX_INLINE_OPS) {
+      int rc = launch_batch(ops + i, std::min(MAX_INLINE_OPS, nops - i), nullptr, 0, device, stream);
+      if (rc != UM_OK) return rc;
+    }
+    return UM_OK;
+  }
+  if (nops > MAX_INLINE_OPS) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    UM_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(UM_ECONTRACT, "a captured one-shot fused launch holds at most " + std::to_string(MAX_INLINE_OPS) +
+                                    " ops (use um_gemm_prepare for longer lists)");
+  }
   Prepared* P = new Prepared();
   int rc = prepare(ops, nops, gets, ngets, device, false, stream, P);
   if (rc == UM_OK) rc = launch_prepared(P, stream);

@@ -25,6 +25,7 @@ import torch
 from paper_2510_08874_b200 import engine as eng
 from paper_2510_08874_b200 import runtime as rt
 from paper_2510_08874_b200.errors import ContractError
+from paper_2510_08874_b200.schedule import schedule_cache
 
 
 class CapturedMultiply:
@@ -64,6 +65,12 @@ class CapturedMultiply:
         self.delta.merge(fab.counters)
         self._sub(self.delta, before)
         self._sub(fab.counters, self.delta)
+        # The graph holds raw addresses of the issue plans' staging buffers and
+        # prepared launches (um_gemm_prepare scratch / descriptor blocks).  Those
+        # live in A's LRU schedule cache for (B, C); pin that cache entry here so
+        # an eviction (A multiplied with many other pairs) cannot free memory a
+        # later replay still reads or writes.
+        self._pinned = schedule_cache(A, B, C)
 
     @staticmethod
     def _sub(a, b):

@@ -320,19 +320,22 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
     if execution == "direct":
         runs = []
         caps = _share_sms(fab, ranks) if cfg.share_sms else {}
-        for r in ranks:
-            sched = lower_direct(A, B, C, cfg, r)
-            _count_reference_traffic(A, B, C, cfg, sched)
-            run = _RankRun(A, B, C, cfg, sched, start)
-            if ovl is not None:
-                # computed once per schedule (the plan built from it is cached too)
-                memo = sched.__dict__.setdefault("signals_memo", {})
-                if id(ovl) not in memo:
-                    memo[id(ovl)] = ovl.signals_for(sched)
-                run.signals, run.signals_key = memo[id(ovl)], ("ovl", id(ovl))
-            runs.append(run.issue())
-        for dev in caps:
-            _capi.check(_capi.load().um_gemm_set_grid_limit(dev, 0), "um_gemm_set_grid_limit")
+        try:
+            for r in ranks:
+                sched = lower_direct(A, B, C, cfg, r)
+                _count_reference_traffic(A, B, C, cfg, sched)
+                run = _RankRun(A, B, C, cfg, sched, start)
+                if ovl is not None:
+                    # computed once per schedule (the plan built from it is cached too)
+                    memo = sched.__dict__.setdefault("signals_memo", {})
+                    if id(ovl) not in memo:
+                        memo[id(ovl)] = ovl.signals_for(sched)
+                    run.signals, run.signals_key = memo[id(ovl)], ("ovl", id(ovl))
+                runs.append(run.issue())
+        finally:
+            # the grid cap is process-global per device: never leave it set
+            for dev in caps:
+                _capi.check(_capi.load().um_gemm_set_grid_limit(dev, 0), "um_gemm_set_grid_limit")
         for run in runs:
             run.stats.flops = int(fab.counters.flops[run.caller])
             results[run.caller] = run.stats
