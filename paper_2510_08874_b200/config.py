@@ -155,3 +155,8 @@ class RunStats:
     staged_bytes: int = 0
     launches: int = 0
     peak_ops_per_launch: int = 0
+    # the order in which the device actually starts the ops (first (sub-)op of
+    # each, as the K1 tile scheduler hands them out): k-chains grouped, pulls
+    # in this order.  executed_ops / a_requests / b_requests keep the
+    # reference's execution order (runtime.py:213-236).
+    device_order: list[LocalMatMulOp] = field(default_factory=list)

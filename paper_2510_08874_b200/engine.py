@@ -254,6 +254,7 @@ class _RankRun:
         st.executed_ops = list(s.ops)
         st.a_requests = [op.a_tile for op in s.ops]
         st.b_requests = [op.b_tile for op in s.ops]
+        st.device_order = [s.ops[i] for i in dict.fromkeys(it[0] for it in items)]
         plan.final_waits = [j for j in range(nf) if not in_kernel[j] and not waited[j]]
         st.peak_inflight_gemms = 1 if s.ops else 0
         return plan
@@ -296,7 +297,7 @@ class _RankRun:
         t = plan.stats
         self.stats = RunStats(list(t.executed_ops), list(t.a_requests), list(t.b_requests), t.peak_inflight_gemms,
                               t.peak_inflight_accums, t.pool_acquired, t.pool_released, t.pool_peak, 0, t.gets,
-                              t.staged_bytes, t.launches, t.peak_ops_per_launch)
+                              t.staged_bytes, t.launches, t.peak_ops_per_launch, list(t.device_order))
 
     def _operand_view(self, name, t, loc, src_idx, staged):
         M = self._mat(name)

@@ -121,6 +121,7 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
         for run in runs:
             st = results[run.caller]
             st.executed_ops += run.stats.executed_ops
+            st.device_order += run.stats.device_order
             st.a_requests += run.stats.a_requests
             st.b_requests += run.stats.b_requests
             st.launches += run.stats.launches

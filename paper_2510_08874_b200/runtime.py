@@ -236,6 +236,7 @@ def run_ir(prog, graph, A, B, C, cfg: ExecConfig, caller: int) -> RunStats:
     _join_current(fab, [done])
     stats.pool_acquired = stats.pool_released = stats.pool_peak = stats.gets
     stats.peak_inflight_gemms = 1 if stats.executed_ops else 0
+    stats.device_order = list(stats.executed_ops)     # IR steps launch in program order
     stats.flops = int(ctr.flops[caller])
     return stats
 

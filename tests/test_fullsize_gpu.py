@@ -9,11 +9,18 @@ every fp32 partial sum < 2**24, so the product is exact):
   (rows of A and columns of B regenerated on the CPU);
 * checksum of checksums: sum_ij C_ij == sum_k (sum_i A_ik)(sum_j B_kj),
   exact in fp64 (|total| < 2**53), so every element of C is covered.
+
+One case (cfg5 at p = 8, the heaviest one-sided traffic) is checked in full:
+all 2^28 entries of C against the oracle's own distributed multiply.  Real
+bf16 inputs are checked on sampled entries for every config.
 """
+
+import os
 
 import numpy as np
 import pytest
 import torch
+from threadpoolctl import threadpool_limits
 
 from oracle import um_oracle as O
 from paper_2510_08874_b200 import ExecConfig, Stationarity, execute_multiply
@@ -86,8 +93,46 @@ def test_fullsize_exact(cuda, name, p):
     assert _total(C) == expect, (name, p)
 
 
+def _dense(seed, rows, cols, mode, block=2048):
+    """The oracle's fill of a whole matrix (fp64), generated in row blocks."""
+    out = np.empty((rows, cols), dtype=np.float64)
+    for r0 in range(0, rows, block):
+        r1 = min(rows, r0 + block)
+        v = O.fill_values(seed, r0, r1, 0, cols, mode)
+        out[r0:r1] = O.round_bf16(v) if mode == "real" else v
+    return out
+
+
+def _gather_c(C) -> np.ndarray:
+    out = np.empty((C.global_shape.rows, C.global_shape.cols), dtype=np.float32)
+    for t in C.grid.tiles():
+        b = C.tile_bounds(t)
+        out[b.rows.lo:b.rows.hi, b.cols.lo:b.cols.hi] = C.segment(t, 0).view2d().cpu().numpy()
+    return out
+
+
+def test_fullsize_all_of_c_against_oracle(cuda):
+    """EVERY element of C at a BASELINE size (cfg5, 16384^3, p = 8 ranks: 32 ops
+    and 496 MiB of one-sided pulls per rank) against the oracle's own
+    distributed multiply (oracle.um_oracle.execute: the reference's op lists,
+    rotation and per-op fp64 GEMMs) on the same integer inputs: bit-exact."""
+    m, n, k, ap, bp, cp, fa, fb, fc = CONFIGS["cfg5"]
+    p = 8
+    fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, 1, 1, 1, seed=SEED, synthetic=True)
+    execute_multiply(A, B, C, ExecConfig(stationarity=Stationarity.STATIONARY_C))
+    torch.cuda.synchronize()
+    got = _gather_c(C)
+    a = _dense(SEED, m, k, "int")
+    b = _dense(SEED + 1, k, n, "int")
+    mats = [O.Mat(nm, r, c, O.resolve_partition(d, r, c, p), 1, p)
+            for nm, (r, c), d in (("A", (m, k), ap), ("B", (k, n), bp), ("C", (m, n), cp))]
+    with threadpool_limits(limits=len(os.sched_getaffinity(0)), user_api="blas"):
+        ref = O.execute("c", *mats, a, b)[0]
+    assert np.array_equal(got.astype(np.float64), ref)
+
+
 @pytest.mark.parametrize("p", [1, 8])
-@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
 def test_fullsize_real_inputs_within_tolerance(cuda, name, p):
     """Real uniform(-1, 1) inputs rounded to bf16 (as the north star states), fp32
     accumulation over k up to 65536 (cfg3): sampled entries of C against the fp64

@@ -131,3 +131,19 @@ def test_random_configs_bands_cover_slices(seed, monkeypatch):
         for r in range(p):
             sched, items, bands, need = plan(A, B, C, r, stationarity=st, **kw)
             check_cover(sched, items, bands, need)
+
+
+def test_device_order_keeps_rotation_balance():
+    """cfg5 at p = 8: the reference's rotation makes every schedule position a
+    permutation of B owners (each rank pulls from a different peer,
+    SURVEY §8(e)); the device order (k-chains grouped, plan_bands) keeps it."""
+    A, B, C = problem(16384, 16384, 16384, 8, "2d", "col", "row")
+    dev, ref = {}, {}
+    for r in range(8):
+        s, items, _, _ = plan(A, B, C, r)
+        dev[r] = [B.owner_rank(s.ops[i].b_tile, 0) for i in dict.fromkeys(it[0] for it in items)]
+        ref[r] = [B.owner_rank(op.b_tile, 0) for op in s.ops]
+        assert sorted(dev[r]) == sorted(ref[r])
+    for order in (dev, ref):
+        for pos in range(len(order[0])):
+            assert len({order[r][pos] for r in range(8)}) == 8, pos
