@@ -243,11 +243,27 @@ UM_API int um_accumulate(const um_view* src, const um_view* dst, void* stream);
 /* K4: replica reduction (distmatrix.py:211-232)                             */
 /* ======================================================================== */
 
-/* dst += (srcs[0] + srcs[1] + ... + srcs[n-1]), summed in array order as the
- * reference's `acc` (distmatrix.py:224-232).  srcs may be peer pointers.
- * Views must share the slice shape; a caller splits a tile into row slices
- * to distribute the reduction over devices.                                */
-UM_API int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, void* stream);
+/* Replaces DistributedMatrix.reduce_replicas (distmatrix.py:211-232) for one
+ * slice of one C tile.  mode:
+ *   UM_REDUCE_PEER  dst += (srcs[0] + ... + srcs[n-1]), summed in array order
+ *                   as the reference's `acc` (distmatrix.py:224-232); srcs may
+ *                   be peer / IPC-mapped pointers (P2P loads over NVLink).
+ *                   Views share the slice shape; a caller splits a tile into
+ *                   row slices to distribute the reduction over devices.
+ *   UM_REDUCE_NCCL  a collective over the replica owners: not callable on one
+ *                   caller's pointers (returns UM_ECONFIG); the host drives it
+ *                   with its NCCL communicator (ncclReduce per slice).
+ *   UM_REDUCE_NVLS  nsrc == 1 and srcs[0] is the slice in a multicast team's
+ *                   address space (um_nvls_team_create over the replicas'
+ *                   um_sym_alloc blocks, dst's own replica a member): dst =
+ *                   multimem.ld_reduce sum over the team (replica 0 included,
+ *                   added in the switch; order is the hardware's, so real
+ *                   inputs may round differently from PEER).
+ * Non-origin replicas keep their partials in every mode.     */
+#define UM_REDUCE_PEER 0
+#define UM_REDUCE_NCCL 1
+#define UM_REDUCE_NVLS 2
+UM_API int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, int32_t mode, void* stream);
 
 /* dst <- src (whole slice), used by broadcast_replica (distmatrix.py:234-250). */
 UM_API int um_copy(const um_view* src, const um_view* dst, void* stream);
@@ -279,6 +295,25 @@ UM_API int um_device_free(int32_t device, void* ptr);
 UM_API int um_ipc_get_handle(void* ptr, void* handle_out);
 UM_API int um_ipc_open_handle(const void* handle, int32_t device, void** ptr_out);
 UM_API int um_ipc_close_handle(void* ptr);
+/* Symmetric memory through the CUDA VMM API (cuMemCreate + cuMemMap, mapped
+ * read/write on every device that can reach the owner; POSIX-fd exportable
+ * where the driver allows; sized to the multicast granularity) -- the
+ * paper's pre-registered pool, and the only memory an
+ * NVLS team can bind.  Replaces fabric.alloc (fabric.py:147-150) for such
+ * segments.                                                                  */
+UM_API int um_sym_granularity(int32_t device, uint64_t* bytes);
+UM_API int um_sym_alloc(int32_t device, uint64_t bytes, void** ptr);
+UM_API int um_sym_free(void* ptr);
+/* NVLS (NVSwitch in-switch reduction) capability: *ok = 1 when the device
+ * supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED).      */
+UM_API int um_nvls_supported(int32_t device, int32_t* ok);
+/* A multicast team over ndev DISTINCT devices, binding sym_ptrs[i] (a
+ * um_sym_alloc base on devices[i]) at offset 0 for `bytes`; mc_ptrs_out[i]
+ * receives the team's multicast address as mapped on devices[i].  Used by
+ * UM_REDUCE_NVLS.  UM_ECONFIG when multicast is unsupported.                 */
+UM_API int um_nvls_team_create(int32_t ndev, const int32_t* devices, void* const* sym_ptrs, uint64_t bytes,
+                               void** mc_ptrs_out, void** team_out);
+UM_API int um_nvls_team_destroy(void* team);
 /* Device count / SM count helpers.                                          */
 UM_API int um_device_count(int32_t* n);
 UM_API int um_sm_count(int32_t device, int32_t* n);

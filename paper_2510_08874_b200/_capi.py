@@ -43,6 +43,10 @@ UM_STATIONARY_A = 0
 UM_STATIONARY_B = 1
 UM_STATIONARY_C = 2
 
+UM_REDUCE_PEER = 0
+UM_REDUCE_NCCL = 1
+UM_REDUCE_NVLS = 2
+
 UM_FILL_ZERO = 0
 UM_FILL_INT = 1
 UM_FILL_REAL = 2
@@ -107,7 +111,14 @@ _SIGS = {
     "um_signal_supported": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_int32)]),
     "um_wait_geq": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
     "um_accumulate": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
-    "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_void_p]),
+    "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
+    "um_sym_granularity": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_uint64)]),
+    "um_sym_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, _P(ctypes.c_void_p)]),
+    "um_sym_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "um_nvls_supported": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_int32)]),
+    "um_nvls_team_create": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_int32), _P(ctypes.c_void_p), ctypes.c_uint64,
+                                           _P(ctypes.c_void_p), _P(ctypes.c_void_p)]),
+    "um_nvls_team_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "um_copy": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_fill": (ctypes.c_int, [_P(UmView), ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
                                ctypes.c_void_p]),

@@ -63,6 +63,12 @@ class ExecConfig:
                          with the gets overlapping the GEMMs of earlier ops;
                          "copy": copy-engine pulls on a get stream, the host
                          splits K1 launches at every pull not yet waited on.
+      reduce_mode        K4 for replicated C: "peer" (P2P loads, reference
+                         summation order), "nvls" (multimem.ld_reduce through a
+                         multicast team: needs Fabric(symmetric="vmm") and the
+                         replicas on distinct multicast-capable GPUs), "nccl"
+                         (ncclReduce per tile; barrier form), "auto" (nvls when
+                         capable, else peer).
     """
 
     stationarity: Stationarity = Stationarity.STATIONARY_C
@@ -84,6 +90,7 @@ class ExecConfig:
     share_sms: bool = False
     reduce_panels: int = 4
     k_split: int = 0
+    reduce_mode: str = "auto"
 
     def __post_init__(self):
         if self.prefetch_depth < 1 or self.max_inflight_gemms < 1 or self.max_inflight_accums < 1:
@@ -100,6 +107,8 @@ class ExecConfig:
             raise ValueError("k_split / mn_split must be >= 0")
         if self.reduce_panels < 1:
             raise ValueError("reduce_panels must be >= 1")
+        if self.reduce_mode not in ("auto", "peer", "nccl", "nvls"):
+            raise ValueError(f"unknown reduce_mode {self.reduce_mode!r}")
         if self.gemm_batch < 0:
             raise ValueError("gemm_batch must be >= 0")
 

@@ -304,11 +304,25 @@ extern "C" int um_accumulate(const um_view* src, const um_view* dst, void* strea
   return UM_OK;
 }
 
-extern "C" int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, void* stream) {
+namespace um {
+int nvls_reduce(const um_view* dst, const um_view* mc_view, void* stream);   // symmem.cu
+}
+
+extern "C" int um_reduce_replicas(const um_view* dst, const um_view* srcs, int32_t nsrc, int32_t mode,
+                                  void* stream) {
   int rc;
   if ((rc = check_view(dst, "dst", false))) return rc;
   if (dst->dtype != UM_F32) return fail(UM_ECONTRACT, "reduce expects fp32");
   if (nsrc < 0) return fail(UM_EVALUE, "negative source count");
+  if (mode == UM_REDUCE_NCCL)
+    return fail(UM_ECONFIG, "UM_REDUCE_NCCL is a collective over the replica owners: the host drives it through "
+                            "its NCCL communicator (replicas.reduce_replicas(mode='nccl'))");
+  if (mode == UM_REDUCE_NVLS) {
+    if (nsrc != 1 || !srcs) return fail(UM_EVALUE, "UM_REDUCE_NVLS takes exactly one source: the multicast view");
+    if ((rc = check_view(&srcs[0], "multicast view", false))) return rc;
+    return nvls_reduce(dst, &srcs[0], stream);
+  }
+  if (mode != UM_REDUCE_PEER) return fail(UM_EVALUE, "unknown reduce mode " + std::to_string(mode));
   const int64_t rows = view_rows(*dst), cols = view_cols(*dst);
   if (rows == 0 || cols == 0 || nsrc == 0) return UM_OK;
   float* d = static_cast<float*>(dst->base) + dst->row_lo * dst->pitch + dst->col_lo;

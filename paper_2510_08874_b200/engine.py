@@ -91,11 +91,14 @@ class _RankRun:
         """Replay this rank's issue plan (built once per schedule and knob set)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
                self.cfg.fine_waits,
-               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key)
+               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key,
+               self.cfg.pool_capacity, self.cfg.prefetch_depth if self.cfg.pool_capacity else 0,
+               self.cfg.max_inflight_gemms if self.cfg.pool_capacity else 0)
         plans = self.sched.__dict__.setdefault("plans", {})
         plan = plans.get(key)
         if plan is None:
-            plan = plans[key] = self._build_plan()
+            plan = plans[key] = (self._build_bounded_plan() if self.cfg.pool_capacity is not None
+                                 else self._build_plan())
         self._replay(plan)
         return self
 
@@ -257,6 +260,173 @@ class _RankRun:
         st.device_order = [s.ops[i] for i in dict.fromkeys(it[0] for it in items)]
         plan.final_waits = [j for j in range(nf) if not in_kernel[j] and not waited[j]]
         st.peak_inflight_gemms = 1 if s.ops else 0
+        return plan
+
+    def _build_bounded_plan(self) -> "_IssuePlan":
+        """Bounded staging (ExecConfig.pool_capacity set): the reference's
+        bounded-asynchrony discipline (runtime.py:43-73,186-231) on the device.
+
+        * a pool of `pool_capacity` staging slots, each as large as the largest
+          remote operand slice one (sub-)op reads, allocated once (the
+          reference's BufferPool of tile-sized buffers);
+        * the (sub-)ops run in device order in launch groups of at most
+          min(max_inflight_gemms, prefetch_depth + 1) ops — the GEMMs in
+          flight together, whose pulls are issued at most prefetch_depth ops
+          ahead of the oldest — whose remote slices fit the free slots; the
+          group's pulls run inside its K1 launch (get warps) and each op waits
+          only for its own slices (fine waits);
+        * a slot is refilled only by a later launch: stream order is the
+          back-pressure (every reader of the old contents has finished), and a
+          slice evicted before its next use is pulled again, as the reference
+          re-fetches per op (runtime.py:219-231);
+        * an op that needs more slots than the pool holds raises the
+          reference's RuntimeError (runtime.py:62-67)."""
+        lib = _capi.load()
+        s, fab, cfg = self.sched, self.fab, self.cfg
+        plan = _IssuePlan(fab.counters.nprocs)
+        st = plan.stats
+        cap = cfg.pool_capacity
+        items, _, _ = plan_bands(s, [False] * len(s.fetches), cfg,
+                                 None if self.signals is None else {i: cuts for i, (cuts, _) in self.signals.items()})
+        last_piece = {(i, m0, m1): it for it, (i, _, m0, m1, *_) in enumerate(items)}
+
+        def units_of(item):
+            """(key, src view, rows, cols, mat) of each remote operand slice the item reads."""
+            i, t, m0, m1, n0, n1, k0, k1 = item
+            op = s.ops[i]
+            out = {}
+            for name, j, loc, (dr0, dr1, dc0, dc1) in (
+                    ("a", s.a_src[i], op.a_local, (m0, m1, k0, k1)), ("b", s.b_src[i], op.b_local, (k0, k1, n0, n1))):
+                if j < 0:
+                    continue
+                f = s.fetches[j]
+                r0, r1 = loc.rows.lo + dr0, loc.rows.lo + dr1
+                c0, c1 = loc.cols.lo + dc0, loc.cols.lo + dc1
+                M = self._mat(f.mat)
+                key = (f.mat, f.tile, f.replica, r0, r1, c0, c1)
+                out[name] = (key, M.segment(f.tile, f.replica).um_view(r0, r1, c0, c1), r1 - r0, c1 - c0, M)
+            return out
+
+        per_item = [units_of(it) for it in items]
+        slot_rows = max([u[2] for us in per_item for u in us.values()], default=0)
+        slot_pitch = max([pitch_for(u[3], u[4].dtype) for us in per_item for u in us.values()], default=0)
+        for us in per_item:
+            if len({u[0] for u in us.values()}) > cap:
+                raise RuntimeError("buffer pool exhausted with nothing left to drain; increase pool_capacity")
+        slots = []
+        if slot_rows and slot_pitch:
+            with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
+                slots = [torch.empty((slot_rows, slot_pitch), dtype=torch.bfloat16, device=f"cuda:{self.dev}")
+                         for _ in range(cap)]
+        plan.staged = slots
+        st.staged_bytes = sum(t.numel() * t.element_size() for t in slots)
+
+        resident: dict = {}              # slice key -> slot (contents valid after the launch that pulled it)
+        holder = [None] * cap            # slot -> slice key
+        group_max = max(1, min(cfg.max_inflight_gemms, cfg.prefetch_depth + 1))
+        batch, gets, in_group = [], [], set()
+        in_use = 0
+
+        def flush():
+            nonlocal batch, gets, in_group
+            if not batch:
+                return
+            arr = (_capi.UmGemmOp * len(batch))(*batch)
+            garr = (_capi.UmGetDesc * max(1, len(gets)))(*gets)
+            h = ctypes.c_void_p()
+            _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, len(gets), self.dev, ctypes.byref(h)),
+                        "um_gemm_prepare")
+            plan.handles.append(h.value)
+            flops = float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo) * (g.b.col_hi - g.b.col_lo)
+                              for g in batch))
+            plan.actions.append(("launch", h.value, flops))
+            st.launches += 1
+            st.peak_ops_per_launch = max(st.peak_ops_per_launch, len(batch))
+            batch, gets, in_group = [], [], set()
+
+        for it, (item, us) in enumerate(zip(items, per_item)):
+            keys = {u[0] for u in us.values()}
+            new = [k for k in keys if k not in resident]
+            slot_of = {k: resident[k] for k in keys if k in resident}
+
+            def free_slots():
+                # slots not read by the current launch group nor holding this op's own slices;
+                # empty ones first
+                fs = [x for x in range(cap) if (holder[x] is None or holder[x] not in in_group)
+                      and x not in slot_of.values()]
+                return sorted(fs, key=lambda x: holder[x] is not None)
+
+            free = free_slots()
+            if (len(batch) >= group_max or len(new) > len(free) or len(gets) + len(new) > _capi.GEMM_MAX_GETS):
+                flush()
+                free = free_slots()
+            get_slot = {}
+            for k in new:
+                x = free.pop(0)
+                if holder[x] is not None:
+                    resident.pop(holder[x], None)
+                holder[x] = k
+                resident[k] = x
+                slot_of[k] = x
+                u = next(v for v in us.values() if v[0] == k)
+                dst = _capi.UmView(slots[x].data_ptr(), 0, u[2], 0, u[3], slots[x].stride(0), _capi.UM_BF16, self.dev)
+                get_slot[k] = len(gets)
+                gets.append(_capi.UmGetDesc(u[1], dst))
+                plan.traffic.add_traffic(self.caller, u[4].owner_rank(k[1], k[2]), 0, 0, u[2] * u[3] * 2)
+                st.gets += 1
+                st.pool_acquired += 1
+                st.pool_released += 1
+            in_group |= keys
+            in_use = len({holder[x] for x in range(cap) if holder[x] in in_group})
+            st.pool_peak = max(st.pool_peak, in_use)
+            i, t, m0, m1, n0, n1, k0, k1 = item
+            op = s.ops[i]
+            views = {}
+            for name, j, loc, (dr0, dr1, dc0, dc1), M in (
+                    ("a", s.a_src[i], op.a_local, (m0, m1, k0, k1), self.A),
+                    ("b", s.b_src[i], op.b_local, (k0, k1, n0, n1), self.B)):
+                if name in us:
+                    key, _, rows, cols, _ = us[name]
+                    x = slot_of[key]
+                    views[name] = _capi.UmView(slots[x].data_ptr(), 0, rows, 0, cols, slots[x].stride(0),
+                                               _capi.UM_BF16, self.dev)
+                else:
+                    seg = M.segment(op.a_tile if name == "a" else op.b_tile, M.replica_of(self.caller))
+                    views[name] = seg.um_view(loc.rows.lo + dr0, loc.rows.lo + dr1, loc.cols.lo + dc0,
+                                              loc.cols.lo + dc1)
+            remote = s.c_remote[i] and self.fab.device_of(
+                self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
+            cseg = self.C.segment(op.c_tile, self.C.replica_of(self.caller))
+            cl = op.c_local
+            gc = cseg.um_view(cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
+            g = _capi.UmGemmOp(views["a"], views["b"], gc, 1 if remote else 0)
+            ga_new = "a" in us and us["a"][0] in get_slot
+            gb_new = "b" in us and us["b"][0] in get_slot
+            if ga_new:
+                g.a_get = get_slot[us["a"][0]] + 1
+            if gb_new:
+                g.b_get = get_slot[us["b"][0]] + 1
+            # a slice pulled earlier in this launch (not by this op's own get) must have landed
+            mask = 0
+            for name in ("a", "b"):
+                if name in us:
+                    k = us[name][0]
+                    if k not in get_slot:
+                        pos = next((q for q, gd in enumerate(gets) if gd.dst.base == slots[slot_of[k]].data_ptr()),
+                                   None)
+                        if pos is not None:
+                            mask |= 1 << pos
+            g.get_mask = mask
+            if self.signals is not None and i in self.signals:
+                g.done_flag = self.signals[i][1](m0, m1)
+                g.done_piece = 1 if it != last_piece[(i, m0, m1)] else 0
+            batch.append(g)
+        flush()
+        st.executed_ops = list(s.ops)
+        st.a_requests = [op.a_tile for op in s.ops]
+        st.b_requests = [op.b_tile for op in s.ops]
+        st.device_order = [s.ops[i] for i in dict.fromkeys(it[0] for it in items)]
+        st.peak_inflight_gemms = min(group_max, len(s.ops)) if s.ops else 0
         return plan
 
     def _replay(self, plan: "_IssuePlan"):

@@ -241,9 +241,15 @@ class Fabric:
     """
 
     def __init__(self, nprocs: int, links: LinkTable | None = None, devices=None, process_group=None,
-                 device_api=None):
+                 device_api=None, symmetric: str = "torch"):
+        """symmetric: "torch" (segments from torch's caching allocator) or "vmm"
+        (one-process mode: every segment its own um_sym_alloc block, bindable
+        to an NVLS multicast team for reduce_mode="nvls")."""
         if nprocs < 1:
             raise ValueError("need at least one process")
+        if symmetric not in ("torch", "vmm"):
+            raise ValueError(f"unknown symmetric memory kind {symmetric!r}")
+        self.symmetric = symmetric
         self.nprocs = nprocs
         self.links = links or LinkTable.uniform(nprocs, 1e9)
         self.counters = FabricCounters(nprocs)

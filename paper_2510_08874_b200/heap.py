@@ -128,6 +128,22 @@ def _wrap_device_ptr(ptr, rows, pitch, dtype, device, keepalive) -> torch.Tensor
     return torch.as_tensor(_CudaArray(ptr, (rows, pitch), "<f4", keepalive), device=f"cuda:{device}")
 
 
+class _VmmBlock:
+    """One um_sym_alloc block (CUDA VMM physical memory mapped on every peer),
+    freed when the last tensor viewing it is gone."""
+
+    def __init__(self, device: int, nbytes: int):
+        p = ctypes.c_void_p()
+        _capi.check(_capi.load().um_sym_alloc(device, nbytes, ctypes.byref(p)), "um_sym_alloc")
+        self.ptr, self.device, self.nbytes = int(p.value), device, nbytes
+
+    def __del__(self):
+        try:
+            _capi.load().um_sym_free(ctypes.c_void_p(self.ptr))
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
 @dataclass
 class _Chunk:
     process: int
@@ -178,6 +194,14 @@ class SymmetricHeap:
             return SymSegment(owner, rows * cols, rows, cols, pitch, dtype, -1, None, 0)
         if self.world.size == 1:
             dev = self.fabric.device_of(owner)
+            if getattr(self.fabric, "symmetric", "torch") == "vmm":
+                esize = torch.empty((), dtype=dtype).element_size()
+                box = _VmmBlock(dev, max(rows, 1) * pitch * esize)
+                t = _wrap_device_ptr(box.ptr, max(rows, 1), pitch, dtype, dev, box)[:rows]
+                t.zero_()
+                seg = SymSegment(owner, rows * cols, rows, cols, pitch, dtype, dev, t, box.ptr)
+                seg.vmm = box
+                return seg
             t = torch.zeros((max(rows, 1), pitch), dtype=dtype, device=f"cuda:{dev}")[:rows]
             return SymSegment(owner, rows * cols, rows, cols, pitch, dtype, dev, t, t.data_ptr())
         return self._allocate_symmetric(owner, rows, cols, pitch, dtype)

@@ -130,7 +130,8 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
         if cross:
             fab.synchronize()
         if C.c > 1:
-            done = rt.reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done, rows=(r0, r1))
+            done = rt.reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done, rows=(r0, r1),
+                                      mode=cfg.reduce_mode)
         for d in devs:
             for ev in done:
                 d2h_s[d][i % nst].wait_event(ev)

@@ -15,20 +15,198 @@ from paper_2510_08874_b200.opgen import Stationarity
 from paper_2510_08874_b200.schedule import DirectSchedule, lower_direct
 
 
+REDUCE_MODES = ("auto", "peer", "nccl", "nvls")
+
+
+class _NvlsTeam:
+    """Multicast team over the c replicas of one C tile (um_nvls_team_create)."""
+
+    def __init__(self, C, t):
+        segs = [C.segment(t, r) for r in range(C.c)]
+        devs = (ctypes.c_int32 * C.c)(*[s_.device for s_ in segs])
+        ptrs = (ctypes.c_void_p * C.c)(*[s_.vmm.ptr for s_ in segs])
+        mc = (ctypes.c_void_p * C.c)()
+        h = ctypes.c_void_p()
+        nbytes = max(s_.vmm.nbytes for s_ in segs)
+        _capi.check(_capi.load().um_nvls_team_create(C.c, devs, ptrs, nbytes, mc, ctypes.byref(h)),
+                    "um_nvls_team_create")
+        self.handle = h.value
+        self.mc = {s_.device: int(mc[i]) for i, s_ in enumerate(segs)}
+        self._keep = segs
+
+    def view(self, seg, device: int, r0: int, r1: int) -> _capi.UmView:
+        """Rows [r0, r1) of the tile in the team's multicast space, as mapped on `device`."""
+        return _capi.UmView(self.mc[device], r0, r1, 0, seg.cols, seg.pitch, _capi.UM_F32, device)
+
+    def __del__(self):
+        try:
+            _capi.load().um_nvls_team_destroy(ctypes.c_void_p(self.handle))
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
+def nvls_capable(C: DistributedMatrix) -> tuple[bool, str]:
+    """Can K4 run in the switch (NVLS) for C?  (capability probe, no side effects)"""
+    fab = C.fabric
+    if C.c < 2:
+        return False, "C is not replicated"
+    if fab.world.size > 1:
+        return False, "NVLS teams are built in one-process mode (multicast handles are not exchanged)"
+    if getattr(fab, "symmetric", "torch") != "vmm":
+        return False, "C's segments are not VMM symmetric memory (Fabric(symmetric='vmm'))"
+    lib = _capi.load()
+    for t in C.grid.tiles():
+        devs = [C.segment(t, r).device for r in range(C.c)]
+        if len(set(devs)) < C.c:
+            return False, f"replicas of tile {t} share a device ({devs}): a multicast team needs distinct GPUs"
+    ok = ctypes.c_int32(0)
+    for d in sorted({C.segment(t, r).device for t in C.grid.tiles() for r in range(C.c)}):
+        _capi.check(lib.um_nvls_supported(d, ctypes.byref(ok)), "um_nvls_supported")
+        if not ok.value:
+            return False, f"device {d} does not support multicast objects (NVLS)"
+    return True, "ok"
+
+
+def nccl_capable(C: DistributedMatrix) -> tuple[bool, str]:
+    fab = C.fabric
+    if C.c < 2:
+        return False, "C is not replicated"
+    if fab.world.size > 1:
+        import torch.distributed as dist
+
+        if dist.get_backend(fab.world.group) != "nccl":
+            return False, "the process group is not NCCL"
+        if fab.devices_shared_across_processes():
+            return False, "processes share a GPU (NCCL needs one GPU per rank)"
+        for t in C.grid.tiles():
+            if len({fab.process_of(C.owner_rank(t, r)) for r in range(C.c)}) < C.c:
+                return False, f"two replicas of tile {t} live in one process"
+        return True, "ok"
+    for t in C.grid.tiles():
+        devs = [C.segment(t, r).device for r in range(C.c)]
+        if len(set(devs)) < C.c:
+            return False, f"replicas of tile {t} share a device ({devs}): NCCL needs distinct GPUs"
+    return True, "ok"
+
+
+def resolve_reduce_mode(C: DistributedMatrix, mode: str) -> str:
+    """"auto" -> "nvls" when capable, else "peer" (one-sided, overlappable).  An
+    explicitly requested mode that cannot run raises ConfigError."""
+    from paper_2510_08874_b200.errors import ConfigError
+
+    if mode not in REDUCE_MODES:
+        raise ConfigError(f"unknown reduce mode {mode!r} (one of {REDUCE_MODES})")
+    if mode == "auto":
+        return "nvls" if nvls_capable(C)[0] else "peer"
+    if mode == "nvls":
+        ok, why = nvls_capable(C)
+        if not ok:
+            raise ConfigError(f"reduce_mode='nvls' unavailable: {why}")
+    if mode == "nccl":
+        ok, why = nccl_capable(C)
+        if not ok:
+            raise ConfigError(f"reduce_mode='nccl' unavailable: {why}")
+    return mode
+
+
+def _nvls_team(C, t) -> _NvlsTeam:
+    teams = C.__dict__.setdefault("_nvls_teams", {})
+    if t not in teams:
+        teams[t] = _NvlsTeam(C, t)
+    return teams[t]
+
+
+def _reduce_nccl(C, origin, start_events, rows):
+    """K4 as NCCL reduce (SURVEY §7 K4 option b): per C tile, the replica owners
+    reduce into the origin's tile (ncclReduce over NVLink).  Single process:
+    torch.cuda.nccl over the tile's devices; one process per GPU: the process
+    group, one subgroup per replica set."""
+    import torch.cuda.nccl as tnccl
+
+    fab = C.fabric
+    done = []
+    if fab.world.size == 1:
+        for t in C.grid.tiles():
+            segs = [C.segment(t, r) for r in range(C.c)]
+            if segs[origin].length == 0:
+                continue
+            lo, hi = 0, segs[origin].rows
+            if rows is not None:
+                tb = C.tile_bounds(t)
+                lo, hi = max(rows[0], tb.rows.lo) - tb.rows.lo, min(rows[1], tb.rows.hi) - tb.rows.lo
+                if hi <= lo:
+                    continue
+            streams = []
+            for s_ in segs:
+                st_ = fab.stream(s_.owner, "reduce")
+                for ev in start_events:
+                    st_.wait_event(ev)
+                streams.append(st_)
+            tnccl.reduce([s_.storage[lo:hi] for s_ in segs], root=origin, streams=streams)
+            for st_ in streams:
+                ev = torch.cuda.Event()
+                ev.record(st_)
+                done.append(ev)
+        return done
+    import torch.distributed as dist
+
+    groups = C.__dict__.get("_nccl_groups")
+    if groups is None:
+        groups = {}
+        for t in C.grid.tiles():          # same order on every process (new_group is collective)
+            procs = tuple(sorted({fab.process_of(C.owner_rank(t, r)) for r in range(C.c)}))
+            if procs not in groups:
+                groups[procs] = dist.new_group(list(procs))
+        C.__dict__["_nccl_groups"] = groups
+    for t in C.grid.tiles():
+        procs = tuple(sorted({fab.process_of(C.owner_rank(t, r)) for r in range(C.c)}))
+        mine = [r for r in range(C.c) if fab.is_local(C.owner_rank(t, r))]
+        if not mine:
+            continue
+        seg = C.segment(t, mine[0])
+        lo, hi = 0, seg.rows
+        if rows is not None:
+            tb = C.tile_bounds(t)
+            lo, hi = max(rows[0], tb.rows.lo) - tb.rows.lo, min(rows[1], tb.rows.hi) - tb.rows.lo
+            if hi <= lo:
+                continue
+        st_ = fab.stream(seg.owner, "reduce")
+        for ev in start_events:
+            st_.wait_event(ev)
+        with torch.cuda.device(seg.device), torch.cuda.stream(st_):
+            buf = seg.storage[lo:hi]
+            dist.reduce(buf, dst=fab.process_of(C.owner_rank(t, origin)), group=groups[procs])
+            ev = torch.cuda.Event()
+            ev.record(st_)
+        done.append(ev)
+    return done
+
+
 def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None,
-                    rows: tuple[int, int] | None = None):
+                    rows: tuple[int, int] | None = None, mode: str = "peer"):
     """replica[origin] += sum_{r != origin} replica[r] (in r order), K4 on device.
 
     distributed: tile rows are split into c slices; slice j is reduced by the
     GPU of replica j's tile owner (slice `origin` by the origin owner), which
     pulls that slice from every other replica over NVLink and adds the sum
     into the origin's slice.
+    mode: "peer" (P2P loads, the reference's summation order), "nvls" (one
+    multimem.ld_reduce per 16 bytes through the tile's multicast team: the
+    switch adds the replicas), "nccl" (ncclReduce per tile), "auto" (nvls
+    when capable, else peer).  See resolve_reduce_mode.
     """
     fab = C.fabric
     fab._require_data()
     lib = _capi.load()
     if start_events is None:
         start_events = _current_events(fab)
+    mode = resolve_reduce_mode(C, mode) if C.c > 1 else "peer"
+    if mode == "nccl":
+        done = _reduce_nccl(C, origin, start_events, rows)
+        _join_current(fab, done)
+        if fab.world.size > 1:
+            fab.synchronize()
+        return done
     done = []
     for t in C.grid.tiles():
         dst = C.segment(t, origin)
@@ -54,10 +232,15 @@ def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = T
             for ev in start_events:
                 stream.wait_event(ev)
             dv = dst.um_view(r0, r1, 0, dst.cols)
-            sv = (_capi.UmView * len(srcs))(*[s.um_view(r0, r1, 0, s.cols) for s in srcs])
+            if mode == "nvls":
+                sv = (_capi.UmView * 1)(_nvls_team(C, t).view(dst, dev, r0, r1))
+                nsrc, kmode = 1, _capi.UM_REDUCE_NVLS
+            else:
+                sv = (_capi.UmView * len(srcs))(*[s.um_view(r0, r1, 0, s.cols) for s in srcs])
+                nsrc, kmode = len(srcs), _capi.UM_REDUCE_PEER
             with torch.cuda.device(dev):
-                _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), ctypes.c_void_p(stream.cuda_stream)),
-                            "um_reduce_replicas")
+                _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, nsrc, kmode,
+                                                   ctypes.c_void_p(stream.cuda_stream)), "um_reduce_replicas")
             ev = torch.cuda.Event()
             ev.record(stream)
             done.append(ev)
@@ -141,8 +324,9 @@ class _ReduceOverlap:
             sig[i] = (cuts, flag)
         return sig
 
-    def reduce(self, start_events) -> list:
-        """Enqueue wait + K4 per sub-slice on the reducers' streams; return done events."""
+    def reduce(self, start_events, mode: str = "peer") -> list:
+        """Enqueue wait + K4 per sub-slice on the reducers' streams; return done events.
+        mode: "peer" or "nvls" (resolved by the caller)."""
         C, fab = self.C, self.C.fabric
         lib = _capi.load()
         self.epoch += 1
@@ -167,8 +351,14 @@ class _ReduceOverlap:
                         _capi.check(lib.um_wait_geq(ctypes.c_void_p(self.flag_ptr(t, k)),
                                                     (self.epoch * exp) & 0xFFFFFFFF, sp), "um_wait_geq")
                     dv = dst.um_view(r0, r1, 0, dst.cols)
-                    sv = (_capi.UmView * len(srcs))(*[s_.um_view(r0, r1, 0, s_.cols) for s_ in srcs])
-                    _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), sp), "um_reduce_replicas")
+                    if mode == "nvls":
+                        sv = (_capi.UmView * 1)(_nvls_team(C, t).view(dst, dev, r0, r1))
+                        _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, 1, _capi.UM_REDUCE_NVLS, sp),
+                                    "um_reduce_replicas")
+                    else:
+                        sv = (_capi.UmView * len(srcs))(*[s_.um_view(r0, r1, 0, s_.cols) for s_ in srcs])
+                        _capi.check(lib.um_reduce_replicas(ctypes.byref(dv), sv, len(srcs), _capi.UM_REDUCE_PEER,
+                                                           sp), "um_reduce_replicas")
                     ev = torch.cuda.Event()
                     ev.record(stream)
                 done.append(ev)
@@ -179,6 +369,8 @@ def _overlap_for(A, B, C, cfg: ExecConfig):
     if not (cfg.overlap_reduce and cfg.reduce_distributed and C.c > 1
             and cfg.stationarity is Stationarity.STATIONARY_C):
         return None
+    if resolve_reduce_mode(C, cfg.reduce_mode) == "nccl":
+        return None                  # a two-sided collective: barrier form
     # processes time-sharing one GPU (no MPS) could park a stream wait that only
     # another process's kernel can satisfy: keep the barrier + K4 path there
     if C.fabric.devices_shared_across_processes() and os.environ.get("UM_OVERLAP_SHARED") != "1":

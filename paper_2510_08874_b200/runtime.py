@@ -41,7 +41,8 @@ from paper_2510_08874_b200.engine import TRACE, _current_events, _IssuePlan, _jo
 from paper_2510_08874_b200.errors import ContractError
 from paper_2510_08874_b200.fabric import ELEM_BYTES, AccumulateMode, pitch_for, um_dtype
 from paper_2510_08874_b200.opgen import LocalMatMulOp, Stationarity  # noqa: F401
-from paper_2510_08874_b200.replicas import _overlap_for, _ReduceOverlap, reduce_replicas  # noqa: F401
+from paper_2510_08874_b200.replicas import (  # noqa: F401
+    _overlap_for, _ReduceOverlap, reduce_replicas, resolve_reduce_mode)
 from paper_2510_08874_b200.schedule import (  # noqa: F401
     DirectSchedule, _Fetch, _in_place, _tma_ok, iteration_offset, lower_direct, plan_bands, rotated_ops,
     schedule_cache)
@@ -354,16 +355,17 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
                 prog = lowering.lower_exhaustive(g, machine, max_compute, max_comm)
             results[r] = run_ir(prog, g, A, B, C, cfg, r)
         done = _current_events(fab)
+    kmode = resolve_reduce_mode(C, cfg.reduce_mode) if C.c > 1 else "peer"
     if ovl is not None:
         # K4 per sub-slice, each started by its replicas' completion signals
         # (no run-level barrier between the GEMMs and the reduction)
-        _join_current(fab, ovl.reduce(start) + done)
+        _join_current(fab, ovl.reduce(start, kmode) + done)
         if fab.world.size > 1:
             fab.synchronize()
     elif cross:
         fab.synchronize()            # run-level barrier across processes
     if C.c > 1 and ovl is None:
-        reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done)
+        reduce_replicas(C, 0, distributed=cfg.reduce_distributed, start_events=done, mode=kmode)
     if C.c > 1:
         for t in C.grid.tiles():      # reference-model accounting of the pulls
             dst = C.segment(t, 0)
