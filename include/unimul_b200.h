@@ -215,6 +215,12 @@ UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages
  * copy engines of the launching stream's device (the paper's transport,
  * PAPER.md:69).                                                            */
 UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
+/* The same pull requesting the copy engines (cudaMemcpyBatchAsync with
+ * cudaMemcpyFlagPreferOverlapWithCompute): the SM-free transport for pulls a
+ * running K1 waits for through um_signal / um_gemm_op.wait_flag (the
+ * reference's get_async + PendingCopy.wait, fabric.py:177-201,
+ * runtime.py:233-236).  Falls back to um_get inside a graph capture.        */
+UM_API int um_get_ce(const um_view* src, const um_view* dst, void* stream);
 
 /* Arrival flag of a get: write `value` to the device word `flag` in stream
  * order (after everything enqueued before it on `stream`), without using an
@@ -230,6 +236,73 @@ UM_API int um_signal_supported(int32_t device, int32_t* out);
  * cannot starve the kernel that will produce the value).  The consumer side
  * of um_gemm_op.done_flag (K4 waiting for every replica's slice).          */
 UM_API int um_wait_geq(const uint32_t* flag, uint32_t value, void* stream);
+
+/* ======================================================================== */
+/* Whole-multiply launch (runtime.execute_multiply, runtime.py:339-387)       */
+/* ======================================================================== */
+
+/* The reference's ExecConfig (runtime.py:26-40) as the C caller states it;
+ * um_execute validates the counts (ValueError there, UM_EVALUE here).  The
+ * schedule knobs themselves are applied when the plan is built.             */
+typedef struct um_exec_cfg {
+  int32_t stationarity;         /* UM_STATIONARY_A | _B | _C                 */
+  int32_t prefetch_depth;       /* >= 1                                       */
+  int32_t max_inflight_gemms;   /* >= 1                                       */
+  int32_t max_inflight_accums;  /* >= 1                                       */
+  int32_t accumulate_mode;      /* 0 PEER_ATOMIC, 1 LOCK_GET_PUT              */
+  int32_t pool_capacity;        /* 0 = None (fetch-once pool), else >= 3      */
+  int32_t reduce_mode;          /* UM_REDUCE_PEER | UM_REDUCE_NVLS            */
+  int32_t reserved;
+} um_exec_cfg;
+
+#define UM_ACT_LAUNCH    0   /* um_gemm_launch(handle) on the rank's compute stream */
+#define UM_ACT_WAIT_COPY 1   /* compute stream waits for copy `arg` to land           */
+#define UM_ACT_WAIT_FLAG 2   /* compute stream waits until *(uint32*)handle >= arg     */
+typedef struct um_exec_action {
+  int32_t kind;
+  int32_t arg;
+  void* handle;
+} um_exec_action;
+
+/* One rank's serialised issue plan (what run_direct does for a rank,
+ * runtime.py:193-256): copy-engine pulls (um_get, issued first on the rank's
+ * get stream in first-use order) and an ordered action list.  Handles are
+ * um_gemm_prepare'd launches; the caller owns them and every buffer the plan
+ * names until um_sync_all (or the caller's own wait) after the last use.     */
+typedef struct um_rank_plan {
+  int32_t rank;
+  int32_t device;
+  int32_t ncopies;
+  int32_t nactions;
+  const um_get_desc* copies;
+  const um_exec_action* actions;
+} um_rank_plan;
+
+/* One replica-reduction step: um_reduce_replicas(dst, srcs, nsrc, mode) on
+ * `device`, after every rank's plan has completed (the run-level barrier,
+ * runtime.py:376-386).                                                      */
+typedef struct um_reduce_step {
+  um_view dst;
+  const um_view* srcs;
+  int32_t nsrc;
+  int32_t mode;
+  int32_t device;
+  int32_t reserved;
+} um_reduce_step;
+
+/* Issue a whole multiply asynchronously: every rank's plan on library-owned
+ * streams (one compute + one get stream per rank), then the reduction steps.
+ * Ordered after the previous um_execute on the same devices; returns without
+ * host synchronisation.  Replaces execute_multiply's loop over ranks.       */
+UM_API int um_execute(const um_rank_plan* ranks, int32_t nranks, const um_reduce_step* reduces, int32_t nreduce,
+                      const um_exec_cfg* cfg);
+/* Host barrier: wait until everything um_execute issued has completed.     */
+UM_API int um_sync_all(void);
+/* Stream interop: `stream` waits for um_execute's work on `device`
+ * (um_execute_wait), or the next um_execute on `device` starts after the
+ * work queued on `stream` (um_execute_after).                               */
+UM_API int um_execute_wait(void* stream, int32_t device);
+UM_API int um_execute_after(void* stream, int32_t device);
 
 /* ======================================================================== */
 /* K3: one-sided accumulate (fabric.py:203-234, distmatrix.py:170-209)        */

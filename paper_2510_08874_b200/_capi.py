@@ -86,6 +86,33 @@ class UmGetDesc(ctypes.Structure):
     _fields_ = [("src", UmView), ("dst", UmView)]
 
 
+class UmExecCfg(ctypes.Structure):
+    _fields_ = [("stationarity", ctypes.c_int32), ("prefetch_depth", ctypes.c_int32),
+                ("max_inflight_gemms", ctypes.c_int32), ("max_inflight_accums", ctypes.c_int32),
+                ("accumulate_mode", ctypes.c_int32), ("pool_capacity", ctypes.c_int32),
+                ("reduce_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class UmExecAction(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("arg", ctypes.c_int32), ("handle", ctypes.c_void_p)]
+
+
+class UmRankPlan(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("device", ctypes.c_int32), ("ncopies", ctypes.c_int32),
+                ("nactions", ctypes.c_int32), ("copies", ctypes.POINTER(UmGetDesc)),
+                ("actions", ctypes.POINTER(UmExecAction))]
+
+
+class UmReduceStep(ctypes.Structure):
+    _fields_ = [("dst", UmView), ("srcs", ctypes.POINTER(UmView)), ("nsrc", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("device", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+UM_ACT_LAUNCH = 0
+UM_ACT_WAIT_COPY = 1
+UM_ACT_WAIT_FLAG = 2
+
+
 # Exported symbols and their C signatures (kept in sync with the header; the
 # CPU test suite asserts every header declaration is exported and bound).
 _P = ctypes.POINTER
@@ -112,6 +139,11 @@ _SIGS = {
     "um_wait_geq": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
     "um_accumulate": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
+    "um_get_ce": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
+    "um_execute": (ctypes.c_int, [_P(UmRankPlan), ctypes.c_int32, _P(UmReduceStep), ctypes.c_int32, _P(UmExecCfg)]),
+    "um_sync_all": (ctypes.c_int, []),
+    "um_execute_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "um_execute_after": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "um_sym_granularity": (ctypes.c_int, [ctypes.c_int32, _P(ctypes.c_uint64)]),
     "um_sym_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, _P(ctypes.c_void_p)]),
     "um_sym_free": (ctypes.c_int, [ctypes.c_void_p]),

@@ -62,7 +62,12 @@ class ExecConfig:
                          to UM_GEMM_MAX_INLINE_OPS ops / UM_GEMM_MAX_GETS pulls)
                          with the gets overlapping the GEMMs of earlier ops;
                          "copy": copy-engine pulls on a get stream, the host
-                         splits K1 launches at every pull not yet waited on.
+                         splits K1 launches at every pull not yet waited on;
+                         "auto" (default): pulls from the caller's own GPU
+                         in-kernel, pulls from other GPUs on the copy engines
+                         (um_get_ce, no SMs) followed by an arrival flag
+                         (um_signal) that the K1 producer waits on inside the
+                         same launch; "ce": every pull that way.
       reduce_mode        K4 for replicated C: "peer" (P2P loads, reference
                          summation order), "nvls" (multimem.ld_reduce through a
                          multicast team: needs Fabric(symmetric="vmm") and the
@@ -82,7 +87,7 @@ class ExecConfig:
     gemm_batch: int = 0
     fused_accumulate: bool = True
     reduce_distributed: bool = True
-    get_engine: str = "kernel"
+    get_engine: str = "auto"
     mn_split: int = 4
     overlap_reduce: bool = True
     chain_order: bool = True
@@ -101,7 +106,7 @@ class ExecConfig:
             raise ValueError(f"unknown staging mode {self.staging!r}")
         if self.same_device_gets not in ("copy", "direct"):
             raise ValueError(f"unknown same_device_gets {self.same_device_gets!r}")
-        if self.get_engine not in ("kernel", "copy"):
+        if self.get_engine not in ("kernel", "copy", "auto", "ce"):
             raise ValueError(f"unknown get_engine {self.get_engine!r}")
         if self.k_split < 0 or self.mn_split < 0:
             raise ValueError("k_split / mn_split must be >= 0")

@@ -130,9 +130,9 @@ static int granularity_of(int device, size_t* g) {
     CUmulticastObjectProp mp = {};
     mp.numDevices = 1;
     mp.size = *g;
-    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.handleTypes = 0;
     size_t mg = 0;
-    if (d.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS && mg > *g) *g = mg;
+    if (d.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_MINIMUM) == CUDA_SUCCESS && mg > *g) *g = mg;
   }
   return UM_OK;
 }
@@ -307,10 +307,10 @@ extern "C" int um_nvls_team_create(int32_t ndev, const int32_t* devices, void* c
   }
   CUmulticastObjectProp mp = {};
   mp.numDevices = (unsigned)ndev;
-  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.handleTypes = 0;           // one process: the multicast handle is not exported
   size_t mg = 0;
   mp.size = bytes;
-  UM_CU_CHECK(d.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  UM_CU_CHECK(d.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_MINIMUM));
   mp.size = (bytes + mg - 1) / mg * mg;
   for (int i = 0; i < ndev; ++i)
     if (allocs[i].size < mp.size) return fail(UM_EVALUE, "team member smaller than the multicast granularity");
@@ -318,6 +318,10 @@ extern "C" int um_nvls_team_create(int32_t ndev, const int32_t* devices, void* c
   T->size = mp.size;
   T->devices.assign(devices, devices + ndev);
   CUresult r = d.mcCreate(&T->mc, &mp);
+  if (r == CUDA_ERROR_INVALID_VALUE) {     // some drivers want an exportable handle type
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    r = d.mcCreate(&T->mc, &mp);
+  }
   if (r != CUDA_SUCCESS) {
     delete T;
     return cu_fail("cuMulticastCreate", r);

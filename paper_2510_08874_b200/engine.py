@@ -54,6 +54,8 @@ class _IssuePlan:
         self.handles: list = []
         self.traffic = FabricCounters(nprocs)   # wire bytes of the pulls, added per run
         self.stats = RunStats()
+        self.flag = None                  # arrival flag of the flagged copy-engine pulls (device int32)
+        self.flagged: set = set()         # fetches whose arrival K1 observes through `flag`
 
     def __del__(self):
         try:
@@ -89,6 +91,11 @@ class _RankRun:
 
     def issue(self):
         """Replay this rank's issue plan (built once per schedule and knob set)."""
+        self._replay(self.plan())
+        return self
+
+    def plan(self) -> "_IssuePlan":
+        """This rank's issue plan, built once per schedule and knob set (cached on the schedule)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
                self.cfg.fine_waits,
                self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key,
@@ -99,8 +106,7 @@ class _RankRun:
         if plan is None:
             plan = plans[key] = (self._build_bounded_plan() if self.cfg.pool_capacity is not None
                                  else self._build_plan())
-        self._replay(plan)
-        return self
+        return plan
 
     def _build_plan(self) -> "_IssuePlan":
         """Resolve everything host-side once: persistent staging buffers (the
@@ -123,14 +129,29 @@ class _RankRun:
         staged = plan.staged
         views = [(self._operand_view("A", op.a_tile, op.a_local, s.a_src[i], staged),
                   self._operand_view("B", op.b_tile, op.b_local, s.b_src[i], staged)) for i, op in enumerate(s.ops)]
-        # which pulls run inside the K1 launch: every op reading the staged slice
-        # must see a TMA-readable view of it (16-byte column start); the rest go
-        # through the copy engines with host-side ordering
-        in_kernel = [self.cfg.get_engine == "kernel"] * nf
+        # which pulls run inside the K1 launch (get warps) and which on the copy
+        # engines.  get_engine "kernel": all in-kernel; "copy": all copy engine,
+        # the host splitting launches at each pull; "auto": pulls from the
+        # caller's own GPU in-kernel, pulls across GPUs (NVLink) on the copy
+        # engines, each followed by an arrival flag the K1 producer waits on
+        # (one launch, no SM spent on the transfer); "ce": every pull on the
+        # copy engines with flags.  Every op reading an in-kernel or flagged
+        # slice must see a TMA-readable view of it (16-byte column start);
+        # the rest fall back to copy engine + host-side ordering.
+        eng = self.cfg.get_engine
+        shared = fab.world.size > 1 and fab.devices_shared_across_processes()
+
+        def same_gpu(j):
+            d = fab.device_of(s.fetches[j].owner)
+            return d == self.dev or (d < 0 and shared)
+
+        in_kernel = [eng == "kernel" or (eng == "auto" and same_gpu(j)) for j in range(nf)]
+        flagged = [eng in ("auto", "ce") and not in_kernel[j] for j in range(nf)]
         for i in range(len(s.ops)):
             for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
                 if src >= 0 and not _tma_ok(v):
                     in_kernel[src] = False
+                    flagged[src] = False
 
         def fetch_views(j, band=None):
             f = s.fetches[j]
@@ -144,9 +165,16 @@ class _RankRun:
                                         None if self.signals is None else {i: cuts for i, (cuts, _) in
                                                                            self.signals.items()})
 
+        flag_value = {}                  # flagged fetch -> arrival-flag value once it has landed
+        if any(flagged):
+            with torch.cuda.device(self.dev):
+                plan.flag = torch.zeros(4, dtype=torch.int32, device=f"cuda:{self.dev}")
         for j, f in enumerate(s.fetches):
             if not in_kernel[j]:
                 plan.host_fetches.append((j, *fetch_views(j)))
+                if flagged[j]:
+                    flag_value[j] = len(flag_value) + 1
+                    plan.flagged.add(j)
                 nbytes = (f.r1 - f.r0) * (f.c1 - f.c0) * staged[j].element_size()
             else:
                 nbytes = sum((r1 - r0) * (c1 - c0) for r0, r1, c0, c1 in bands[j]) * staged[j].element_size()
@@ -197,8 +225,9 @@ class _RankRun:
         for it, (i, t, m0, m1, n0, n1, k0, k1) in enumerate(items):
             op = s.ops[i]
             srcs = [j for j in (s.a_src[i], s.b_src[i]) if j >= 0]
+            unfused = s.c_remote[i] and not self.cfg.fused_accumulate
             for j in srcs:
-                if not in_kernel[j]:
+                if not in_kernel[j] and (not flagged[j] or unfused):
                     host_wait(j)
             remote = s.c_remote[i] and self.fab.device_of(
                 self.C.owner_rank(op.c_tile, self.C.replica_of(self.caller))) != self.dev
@@ -232,6 +261,10 @@ class _RankRun:
             cl = op.c_local
             gc = cseg.um_view(cl.rows.lo + m0, cl.rows.lo + m1, cl.cols.lo + n0, cl.cols.lo + n1)
             g = _capi.UmGemmOp(ga, gb, gc, 1 if remote else 0)
+            fv = [flag_value[j] for j in srcs if j in flag_value and not waited[j]]
+            if fv:                       # copy-engine pulls: wait on the arrival flag in the kernel
+                g.wait_flag = plan.flag.data_ptr()
+                g.wait_value = max(fv)
             # an operand read from ONE band of this launch (inside its columns)
             # waits chunk by chunk: A for its tile rows, B for each k-block's rows
             fine = {}
@@ -308,15 +341,15 @@ class _RankRun:
             return out
 
         per_item = [units_of(it) for it in items]
-        slot_rows = max([u[2] for us in per_item for u in us.values()], default=0)
-        slot_pitch = max([pitch_for(u[3], u[4].dtype) for us in per_item for u in us.values()], default=0)
+        # a slot holds any one slice (its own 16-byte pitch, rows packed)
+        slot_elems = max([u[2] * pitch_for(u[3], u[4].dtype) for us in per_item for u in us.values()], default=0)
         for us in per_item:
             if len({u[0] for u in us.values()}) > cap:
                 raise RuntimeError("buffer pool exhausted with nothing left to drain; increase pool_capacity")
         slots = []
-        if slot_rows and slot_pitch:
+        if slot_elems:
             with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
-                slots = [torch.empty((slot_rows, slot_pitch), dtype=torch.bfloat16, device=f"cuda:{self.dev}")
+                slots = [torch.empty(slot_elems, dtype=torch.bfloat16, device=f"cuda:{self.dev}")
                          for _ in range(cap)]
         plan.staged = slots
         st.staged_bytes = sum(t.numel() * t.element_size() for t in slots)
@@ -369,7 +402,8 @@ class _RankRun:
                 resident[k] = x
                 slot_of[k] = x
                 u = next(v for v in us.values() if v[0] == k)
-                dst = _capi.UmView(slots[x].data_ptr(), 0, u[2], 0, u[3], slots[x].stride(0), _capi.UM_BF16, self.dev)
+                dst = _capi.UmView(slots[x].data_ptr(), 0, u[2], 0, u[3], pitch_for(u[3], u[4].dtype), _capi.UM_BF16,
+                                   self.dev)
                 get_slot[k] = len(gets)
                 gets.append(_capi.UmGetDesc(u[1], dst))
                 plan.traffic.add_traffic(self.caller, u[4].owner_rank(k[1], k[2]), 0, 0, u[2] * u[3] * 2)
@@ -386,9 +420,9 @@ class _RankRun:
                     ("a", s.a_src[i], op.a_local, (m0, m1, k0, k1), self.A),
                     ("b", s.b_src[i], op.b_local, (k0, k1, n0, n1), self.B)):
                 if name in us:
-                    key, _, rows, cols, _ = us[name]
+                    key, _, rows, cols, Mu = us[name]
                     x = slot_of[key]
-                    views[name] = _capi.UmView(slots[x].data_ptr(), 0, rows, 0, cols, slots[x].stride(0),
+                    views[name] = _capi.UmView(slots[x].data_ptr(), 0, rows, 0, cols, pitch_for(cols, Mu.dtype),
                                                _capi.UM_BF16, self.dev)
                 else:
                     seg = M.segment(op.a_tile if name == "a" else op.b_tile, M.replica_of(self.caller))
@@ -435,8 +469,21 @@ class _RankRun:
         with torch.cuda.device(self.dev):
             events = {}
             gsp = ctypes.c_void_p(self.gs.cuda_stream)
+            if plan.flagged:
+                # reset the arrival flag before this run's K1 can read it
+                fptr = ctypes.c_void_p(plan.flag.data_ptr())
+                _capi.check(lib.um_signal(fptr, 0, gsp), "um_signal")
+                ev = torch.cuda.Event()
+                ev.record(self.gs)
+                self.cs.wait_event(ev)
+            landed = 0
             for j, src, dst in plan.host_fetches:        # K2 on the copy engines, first-use order
-                _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get")
+                if j in plan.flagged:
+                    _capi.check(lib.um_get_ce(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get_ce")
+                    landed += 1
+                    _capi.check(lib.um_signal(fptr, landed, gsp), "um_signal")
+                else:
+                    _capi.check(lib.um_get(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get")
                 ev = torch.cuda.Event()
                 ev.record(self.gs)
                 events[j] = ev

@@ -35,9 +35,9 @@ def test_bounded_pool_exact_and_bounded(cuda, case, cap, depth, inflight):
         assert st.pool_peak <= cap
         assert st.peak_ops_per_launch <= min(inflight, depth + 1)
         # every slot is one op's largest operand slice: staging bounded by the pool
-        max_slice = max((len(op.m_bound) * len(op.k_bound), len(op.k_bound) * len(op.n_bound))
+        max_slice = max(max(len(op.m_bound) * len(op.k_bound), len(op.k_bound) * len(op.n_bound))
                         for op in st.executed_ops) if st.executed_ops else 0
-        assert st.staged_bytes <= cap * max(1, max_slice) * 2 + cap * 1024 * 16
+        assert st.staged_bytes <= cap * max(1, max_slice) * 2 + cap * 1024 * 16     # + pitch padding
         if free[r].gets:
             assert st.gets >= free[r].gets               # evicted slices are pulled again
         assert [o.a_tile for o in st.executed_ops] == [o.a_tile for o in free[r].executed_ops]

@@ -67,3 +67,41 @@ def test_owner_rank_matches_python_tiling():
             for rep in range(2):
                 assert lib.um_owner_rank(ctypes.byref(d), 12, t.i, t.j, rep, ctypes.byref(out)) == 0
                 assert out.value == tiling.owner_of(part, grid, t, 6) + 6 * rep
+
+
+def test_struct_layouts_match_the_c_compiler(tmp_path):
+    """sizeof / offsetof of every header struct, as gcc lays them out, equal the ctypes mirrors."""
+    import shutil
+    import subprocess
+
+    import pytest
+
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    structs = {"um_view": _capi.UmView, "um_mat_desc": _capi.UmMatDesc, "um_gemm_op": _capi.UmGemmOp,
+               "um_get_desc": _capi.UmGetDesc, "um_exec_cfg": _capi.UmExecCfg, "um_exec_action": _capi.UmExecAction,
+               "um_rank_plan": _capi.UmRankPlan, "um_reduce_step": _capi.UmReduceStep}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                     check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
+
+
+def test_execute_validates_without_gpu():
+    lib = _capi.load()
+    assert lib.um_execute(None, -1, None, 0, None) == _capi.UM_EVALUE
+    bad = _capi.UmExecCfg(2, 0, 4, 4, 0, 0, 0, 0)               # prefetch_depth 0: runtime.py:35-37
+    assert lib.um_execute(None, 0, None, 0, ctypes.byref(bad)) == _capi.UM_EVALUE
+    assert "counts must be >= 1" in _capi.last_error()

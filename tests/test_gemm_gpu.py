@@ -141,3 +141,40 @@ def test_wait_flag_orders_op_after_signal(cuda):
     torch.cuda.synchronize()
     assert torch.equal(c, ref_acc(torch.zeros_like(c), a, b))
     assert flag.tolist() == [0, 7, 0, 0]
+
+
+def test_wait_flag_orders_op_after_copy_engine_pull(cuda):
+    """The SM-free get protocol (get_engine auto/ce): a copy-engine pull
+    (um_get_ce, here from pinned host memory so it can only be a copy engine)
+    on a second stream delivers B into a staging buffer, um_signal publishes
+    its arrival, and the K1 producer (already running, holding every SM it
+    wants) waits on the flag before its TMA reads the staged B."""
+    import ctypes
+
+    from paper_2510_08874_b200 import _capi
+
+    lib = _capi.load()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = ints(512, 384, g, torch.bfloat16)
+    b_host = ints(384, 512, g, torch.bfloat16).cpu().pin_memory()
+    staged = torch.zeros(384, 512, dtype=torch.bfloat16, device="cuda")
+    c = torch.zeros(512, 512, device="cuda")
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s_get, s_gemm = torch.cuda.Stream(), torch.cuda.Stream()
+    op = _capi.UmGemmOp(_capi.UmView(a.data_ptr(), 0, 512, 0, 384, a.stride(0), _capi.UM_BF16, 0),
+                        _capi.UmView(staged.data_ptr(), 0, 384, 0, 512, 512, _capi.UM_BF16, 0),
+                        _capi.UmView(c.data_ptr(), 0, 512, 0, 512, c.stride(0), _capi.UM_F32, 0), 0)
+    op.wait_flag = flag.data_ptr()
+    op.wait_value = 1
+    src = _capi.UmView(b_host.data_ptr(), 0, 384, 0, 512, 512, _capi.UM_BF16, -1)
+    dst = _capi.UmView(staged.data_ptr(), 0, 384, 0, 512, 512, _capi.UM_BF16, 0)
+    with torch.cuda.stream(s_get):
+        torch.cuda._sleep(20_000_000)         # the pull starts ~10 ms after K1 is already waiting
+    gsp = ctypes.c_void_p(s_get.cuda_stream)
+    _capi.check(lib.um_get_ce(ctypes.byref(src), ctypes.byref(dst), gsp), "um_get_ce")
+    _capi.check(lib.um_signal(ctypes.c_void_p(flag.data_ptr()), 1, gsp), "um_signal")
+    _capi.check(lib.um_gemm_acc_batch(ctypes.byref(op), 1, 0, ctypes.c_void_p(s_gemm.cuda_stream)),
+                "um_gemm_acc_batch")
+    torch.cuda.synchronize()
+    assert torch.equal(c, ref_acc(torch.zeros_like(c), a, b_host.cuda()))
