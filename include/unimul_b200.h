@@ -378,7 +378,9 @@ UM_API int um_sym_granularity(int32_t device, uint64_t* bytes);
 UM_API int um_sym_alloc(int32_t device, uint64_t bytes, void** ptr);
 UM_API int um_sym_free(void* ptr);
 /* NVLS (NVSwitch in-switch reduction) capability: *ok = 1 when the device
- * supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED).      */
+ * reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED AND a trial multicast
+ * object can be created (a fabric not configured for multicast refuses
+ * cuMulticastCreate although the attribute is set).                         */
 UM_API int um_nvls_supported(int32_t device, int32_t* ok);
 /* A multicast team over ndev DISTINCT devices, binding sym_ptrs[i] (a
  * um_sym_alloc base on devices[i]) at offset 0 for `bytes`; mc_ptrs_out[i]

@@ -20,6 +20,7 @@ import dataclasses
 
 import torch
 
+from paper_2510_08874_b200.trace import nvtx
 from paper_2510_08874_b200 import _capi
 from paper_2510_08874_b200.config import ExecConfig
 from paper_2510_08874_b200.engine import _RankRun
@@ -110,6 +111,7 @@ class CompiledMultiply:
         self.cfg_c = exec_cfg(cfg, _capi.UM_REDUCE_NVLS if mode == "nvls" else _capi.UM_REDUCE_PEER)
         self.devices = sorted({fab.device_of(r) for r in fab.local_ranks()})
 
+    @nvtx("um:um_execute")
     def execute(self, sync: bool = False) -> None:
         """One more C += A @ B: a single um_execute call (ordered after, and
         joined back into, torch's current streams of the devices)."""

@@ -20,6 +20,7 @@
 //   * reduction steps start after every rank's last action (the reference's
 //     run-level barrier before reduce_replicas).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <map>
@@ -79,6 +80,10 @@ extern "C" int um_execute(const um_rank_plan* ranks, int32_t nranks, const um_re
     return fail(UM_EVALUE, "ExecConfig counts must be >= 1");   // runtime.py:35-37
   Streams& st = S();
   std::lock_guard<std::mutex> lk(st.mu);
+  struct Range {   // NVTX range "um:um_execute" around the whole host issue
+    Range() { nvtxRangePushA("um:um_execute"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   int rc;
   std::vector<cudaEvent_t> events;       // destroyed at the end (recorded work keeps running)
   auto cleanup = [&]() {

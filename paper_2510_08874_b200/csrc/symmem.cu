@@ -273,14 +273,43 @@ extern "C" int um_sym_free(void* ptr) {
 }
 
 extern "C" int um_nvls_supported(int32_t device, int32_t* ok) {
+  // The device attribute alone is not enough: a box whose NVSwitch fabric is
+  // not configured for multicast (no fabric manager / IMEX in this container)
+  // reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 1 and then refuses
+  // cuMulticastCreate.  So the probe also creates (and releases) a minimal
+  // multicast object once per device.
   if (!ok) return fail(UM_EVALUE, "null out pointer");
   *ok = 0;
   const Drv& d = drv();
-  if (!d.ok || !d.mcCreate) return UM_OK;
+  if (!d.ok || !d.mcCreate || device < 0 || device >= 64) return UM_OK;
+  static std::mutex mu;
+  static int cache[64];
+  static bool init = false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!init) {
+    for (int& c : cache) c = -1;
+    init = true;
+  }
+  if (cache[device] >= 0) {
+    *ok = cache[device];
+    return UM_OK;
+  }
+  cache[device] = 0;
   CUdevice dev;
   if (d.devGet(&dev, device) != CUDA_SUCCESS) return UM_OK;
   int v = 0;
-  if (d.devAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) == CUDA_SUCCESS) *ok = v ? 1 : 0;
+  if (d.devAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS || !v) return UM_OK;
+  CUmulticastObjectProp mp = {};
+  mp.numDevices = 1;
+  size_t mg = 0;
+  mp.size = 2 << 20;
+  if (d.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_MINIMUM) != CUDA_SUCCESS) return UM_OK;
+  mp.size = mg;
+  CUmemGenericAllocationHandle h;
+  if (d.mcCreate(&h, &mp) != CUDA_SUCCESS) return UM_OK;
+  d.memRelease(h);
+  cache[device] = 1;
+  *ok = 1;
   return UM_OK;
 }
 

@@ -11,6 +11,7 @@ import ctypes
 
 import torch
 
+from paper_2510_08874_b200.trace import nvtx
 from paper_2510_08874_b200 import _capi
 from paper_2510_08874_b200 import schedule as _sch
 from paper_2510_08874_b200.config import ExecConfig, RunStats
@@ -108,6 +109,7 @@ class _RankRun:
                                  else self._build_plan())
         return plan
 
+    @nvtx("um:plan")
     def _build_plan(self) -> "_IssuePlan":
         """Resolve everything host-side once: persistent staging buffers (the
         paper's pre-allocated pool), which pulls run inside
@@ -295,6 +297,7 @@ class _RankRun:
         st.peak_inflight_gemms = 1 if s.ops else 0
         return plan
 
+    @nvtx("um:plan_bounded")
     def _build_bounded_plan(self) -> "_IssuePlan":
         """Bounded staging (ExecConfig.pool_capacity set): the reference's
         bounded-asynchrony discipline (runtime.py:43-73,186-231) on the device.
@@ -463,6 +466,7 @@ class _RankRun:
         st.peak_inflight_gemms = min(group_max, len(s.ops)) if s.ops else 0
         return plan
 
+    @nvtx("um:issue_rank")
     def _replay(self, plan: "_IssuePlan"):
         lib = _capi.load()
         fab = self.fab

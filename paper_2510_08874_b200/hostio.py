@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import torch
 
+from paper_2510_08874_b200.trace import nvtx
 from paper_2510_08874_b200 import runtime as rt
 from paper_2510_08874_b200.errors import ContractError
 from paper_2510_08874_b200.opgen import LocalMatMulOp
@@ -59,6 +60,7 @@ def _copy_rows(M, host: torch.Tensor, r0: int, r1: int, stream_of, to_device: bo
     return fab
 
 
+@nvtx("um:multiply_from_host")
 def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_out: torch.Tensor,
                        cfg: rt.ExecConfig | None = None, panels: int = 8, copy_streams: int = 1) -> dict:
     """C += A @ B with A, B uploaded from host and replica 0 of C downloaded to c_out.

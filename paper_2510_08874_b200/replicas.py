@@ -7,6 +7,7 @@ import os
 
 import torch
 
+from paper_2510_08874_b200.trace import nvtx
 from paper_2510_08874_b200 import _capi
 from paper_2510_08874_b200.config import ExecConfig
 from paper_2510_08874_b200.distmatrix import DistributedMatrix
@@ -182,6 +183,7 @@ def _reduce_nccl(C, origin, start_events, rows):
     return done
 
 
+@nvtx("um:K4_reduce_replicas")
 def reduce_replicas(C: DistributedMatrix, origin: int = 0, distributed: bool = True, start_events=None,
                     rows: tuple[int, int] | None = None, mode: str = "peer"):
     """replica[origin] += sum_{r != origin} replica[r] (in r order), K4 on device.
@@ -324,6 +326,7 @@ class _ReduceOverlap:
             sig[i] = (cuts, flag)
         return sig
 
+    @nvtx("um:K4_overlapped")
     def reduce(self, start_events, mode: str = "peer") -> list:
         """Enqueue wait + K4 per sub-slice on the reducers' streams; return done events.
         mode: "peer" or "nvls" (resolved by the caller)."""

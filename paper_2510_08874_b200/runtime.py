@@ -34,6 +34,7 @@ import ctypes
 
 import torch
 
+from paper_2510_08874_b200.trace import nvtx
 from paper_2510_08874_b200 import _capi, engine, kernels, lowering, opgen
 from paper_2510_08874_b200.config import BufferPool, ExecConfig, RunStats
 from paper_2510_08874_b200.distmatrix import DistributedMatrix
@@ -112,6 +113,7 @@ def _check_operands(A, B, C):
     A.fabric._require_data()
 
 
+@nvtx("um:run_direct")
 def run_direct(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                caller: int) -> RunStats:
     """Direct execution of one rank's rotated op list (runtime.py:193-256).
@@ -136,6 +138,7 @@ def run_direct(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix,
 # IR replay (runtime.py:259-336)
 # ---------------------------------------------------------------------------
 
+@nvtx("um:run_ir")
 def run_ir(prog, graph, A, B, C, cfg: ExecConfig, caller: int) -> RunStats:
     """Replay a validated single-rank IR program on the device.
 
@@ -297,6 +300,7 @@ def _share_sms(fab, ranks) -> dict:
     return caps
 
 
+@nvtx("um:execute_multiply")
 def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                      execution: str = "direct", machine=None, max_compute: int | None = None,
                      max_comm: int | None = None, threaded: bool = False) -> dict[int, RunStats]:
