@@ -173,6 +173,31 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
   }
 }
 
+// Staggered start (stream-K start, `nstag` > 0): work unit u < total_tiles is
+// tile u, except that the first nstag tiles run only a prefix [0, L) of their
+// k-blocks, L growing from 1 to num_kb - 1 across them; units total_tiles ..
+// total_tiles + nstag - 1 are those tiles' remainders [L, num_kb).  The first
+// wave's pairs thus finish their first unit at evenly spread times, so tile
+// ends (and their C read-modify-write bursts) stay spread over the whole run
+// instead of every pair draining at once each wave, and the remainders fill
+// the last wave (list scheduling then ends within one k-block-sized piece of
+// the ideal T / pairs).  Both pieces reduce-add into C (atomic), so they need
+// no ordering.  Returns the tile index; [kb0, kb1) is the unit's k range.
+__device__ __forceinline__ int unit_span(const Work* works, int nwork, int total_tiles, int nstag, int u, int& w,
+                                         int& kb0, int& kb1) {
+  const int t = u >= total_tiles ? u - total_tiles : u;
+  w = find_work(works, nwork, t);
+  const int kb = works[w].num_kb;
+  kb0 = 0;
+  kb1 = kb;
+  if (t < nstag) {
+    const int L = 1 + (int)(((long long)t * (kb - 1)) / nstag);
+    if (u >= total_tiles) kb0 = L;
+    else kb1 = L;
+  }
+  return t;
+}
+
 // Dynamic tile scheduling: the leader producer of each cluster takes the next
 // tile index from a global atomic counter and broadcasts it through a small
 // ring in shared memory (written into both CTAs of the pair) to every role.
@@ -222,6 +247,8 @@ struct alignas(64) LaunchArgs {
   int* counters;              // per-stream {tile, done clusters, get chunk, get done[MAX_GETS]}
   int ngets, total_chunks;
   int nslots;
+  int nstag;                  // staggered start: the first nstag tiles run a k-prefix, their rest comes last
+  int stag_ok;                // host: this launch may use a staggered start (set at prepare)
   uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
   unsigned long long* prof;   // (profiling, UM_GEMM_STALLS) per cluster: MMA-thread cycles total / waiting
                               // for operands / for the epilogue to free TMEM / for the next tile
@@ -247,6 +274,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   const CUtensorMap* __restrict__ maps = args.maps ? args.maps : args.inl_maps;
   const int nwork = args.nwork;
   const int total_tiles = args.total_tiles;
+  const int nstag = args.nstag;
+  const int total_units = total_tiles + nstag;   // work units handed out by the tile scheduler
   int* const tile_counter = args.counters;       // [0] next tile, [1] finished clusters
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -390,7 +419,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           } else {
             int t = (NP == 1 && works[0].sched_static) ? (int)(blockIdx.x / CS) + i * (int)(gridDim.x / CS)  // A/B knob
                                                        : atomicAdd(tile_counter, 1);
-            if (t > total_tiles) t = total_tiles;
+            if (t > total_units) t = total_units;
             q = t * NP;
           }
           tq[slot] = q;
@@ -406,7 +435,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         int t, row_off;
         decode(q, t, row_off);
         if (i == 0) stamp(2);
-        if (t >= total_tiles) {
+        if (t >= total_units) {
           if (leader) {
             // this pair is done with the counter (its cluster leader took its
             // last tile); the last pair out re-zeroes it for the next launch
@@ -418,7 +447,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           }
           break;
         }
-        const int w0 = find_work(works, nwork, t);
+        int w0, ukb0, ukb1;
+        t = unit_span(works, nwork, total_tiles, nstag, t, w0, ukb0, ukb1);
         int mb, nb;
         tile_coords(works[w0], t - works[w0].tile_start, mb, nb);
         // a k-chain: the segments (ops with the same C region) are loaded one
@@ -456,9 +486,12 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, wk.b_row0 + kb * BK);
         };
         const int pf = wk.prefetch;
-        for (int kb = 0; kb < min(pf, wk.seg_kb); ++kb) prefetch(kb);
-        for (int kb = 0; kb < wk.seg_kb; ++kb) {
-          if (pf > 0 && kb + pf < wk.seg_kb) prefetch(kb + pf);
+        // k-blocks of this segment; a staggered unit (single-segment works only)
+        // covers [ukb0, ukb1) of its tile
+        const int kbs = nstag ? ukb0 : 0, kbe = nstag ? ukb1 : wk.seg_kb;
+        for (int kb = kbs; kb < min(kbs + pf, kbe); ++kb) prefetch(kb);
+        for (int kb = kbs; kb < kbe; ++kb) {
+          if (pf > 0 && kb + pf < kbe) prefetch(kb + pf);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           // (profiling only, UM_GEMM_DEBUG_HALFB: wrong results) skip the second
           // accumulator's B sub-tiles -> bound on what halving B traffic can buy
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         int t = 0, row_off_unused;
         timed(c_tile, [&] { t = next_tile(it); });
         decode(t, t, row_off_unused);
-        if (t >= total_tiles) break;
+        if (t >= total_units) break;
 #if UM_PROFILE
         const int tl_pair = (int)(blockIdx.x / CG);
         if (args.prof && it < TL_TILES && tl_pair < 128) {
@@ -562,8 +595,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           e[1] = ptx::globaltimer();
         }
 #endif
-        const int w = find_work(works, nwork, t);
-        const int num_kb = works[w].num_kb;
+        int w, ukb0, ukb1;
+        t = unit_span(works, nwork, total_tiles, nstag, t, w, ukb0, ukb1);
+        const int num_kb = ukb1 - ukb0;    // k-blocks of this unit (the whole chain's, unstaggered)
         const int buf = it % C::NBUF;
         const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
         if constexpr (C::NACC == 1) {
@@ -658,8 +692,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       int t = 0, row_off;
       if (lane == 0) t = next_tile(it);
       decode(__shfl_sync(0xffffffffu, t, 0), t, row_off);
-      if (t >= total_tiles) break;
-      const int w = find_work(works, nwork, t);
+      if (t >= total_units) break;
+      int w, ukb0_unused, ukb1_unused;
+      t = unit_span(works, nwork, total_tiles, nstag, t, w, ukb0_unused, ukb1_unused);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
       if (wk.c_pol >= 0) cpol = cpols[wk.c_pol];
@@ -967,6 +1002,7 @@ struct Knobs {
   int tail_split = 0;
   int cpf = 0;
   int stagger = 0;
+  int skstart = 1;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -989,6 +1025,7 @@ static const Knobs& knobs() {
     k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
+    k.skstart = env_int("UM_GEMM_SKSTART", 1) ? 1 : 0;
   });
   return k;
 }
@@ -1066,6 +1103,8 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
     occ[device] = (e == cudaSuccess && n > 0) ? n : 1;
   }
   if (NP > 1 && fixed) units = std::min(units, occ[device] * NP);
+  // staggered start over the first wave: one prefix per launched pair
+  args.nstag = (NP == 1 && args.stag_ok && total_tiles >= units) ? units : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
@@ -1496,6 +1535,14 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   args.nwork = (int)works.size();
   args.total_tiles = total;
   args.nslots = (int)slot_flags.size();
+  // staggered start (unit_span): plain launches only -- no in-kernel gets, no
+  // completion slots (a split tile is written twice), no k-chains, and tiles
+  // long enough (>= 8 k-blocks) that a prefix/remainder pair stays mainloop-bound
+  {
+    bool ok = kn.skstart && ngets == 0 && args.nslots == 0 && !works.empty();
+    for (const Work& w : works) ok = ok && w.nseg == 1 && w.num_kb >= 8;
+    args.stag_ok = ok ? 1 : 0;
+  }
   for (int s = 0; s < args.nslots; ++s) args.slots[s] = {slot_flags[s], slot_expected[s], slot_inc[s]};
   // ---- in-kernel gets (fused K2)
   int chunks = 0;
