@@ -67,7 +67,7 @@ typedef struct {
  * [row_lo,row_hi) x [col_lo,col_hi) in tile-local coordinates.  This is the
  * form the TMA tensor maps consume directly (base = tile base, dims =
  * (col_hi,row_hi), start = (col_lo,row_lo)), so unaligned slices need no copy.
- * Replaces the numpy slice views of runtime.py:351-358 / kernels.py:13-17.
+ * Replaces the numpy slice views of runtime.py:143-150 / kernels.py:13-17.
  */
 typedef struct {
   void*   base;                  /* tile base (local, peer-mapped or IPC-mapped) */
@@ -102,7 +102,7 @@ UM_API int um_plan(const um_mat_desc* A, const um_mat_desc* B, const um_mat_desc
             int32_t nprocs, int32_t stationarity, int32_t caller,
             int64_t* ops_out, int64_t cap, int64_t* n_out);
 
-/* iteration_offset(stationary_tile, nops)  (runtime.py:89-93 / 297-301).  */
+/* iteration_offset(stationary_tile, nops)  (runtime.py:89-93).  */
 UM_API int um_iteration_offset(int64_t ti, int64_t tj, int64_t nops, int64_t* out);
 
 /* tiling.owner_of + DistributedMatrix.owner_rank (tiling.py:206-221,

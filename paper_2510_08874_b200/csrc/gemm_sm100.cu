@@ -1103,8 +1103,16 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
     occ[device] = (e == cudaSuccess && n > 0) ? n : 1;
   }
   if (NP > 1 && fixed) units = std::min(units, occ[device] * NP);
-  // staggered start over the first wave: one prefix per launched pair
-  args.nstag = (NP == 1 && args.stag_ok && total_tiles >= units) ? units : 0;
+  // staggered start over the first wave (one prefix per launched pair) only
+  // where the last wave would otherwise leave > 10 % of the launch idle: the
+  // split tiles cost an extra epilogue and pipeline refill each (measured on
+  // one B200: 4096^3 +9 %, but 8192^3 -2 %, 16384^3 -3 %, 6144^3 -8 % when
+  // applied everywhere; tools/k1_ab.py, profiles/r2_ab_skstart.json)
+  {
+    const int waves = (total_tiles + units - 1) / max(1, units);
+    const double idle = waves > 0 ? 1.0 - (double)total_tiles / ((double)waves * units) : 0.0;
+    args.nstag = (NP == 1 && args.stag_ok && total_tiles > units && idle > 0.10) ? units : 0;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);

@@ -258,7 +258,7 @@ extern "C" int um_plan(const um_mat_desc* Ad, const um_mat_desc* Bd, const um_ma
 }
 
 extern "C" int um_iteration_offset(int64_t ti, int64_t tj, int64_t nops, int64_t* out) {
-  if (nops < 1) return fail(UM_EVALUE, "nops must be >= 1");  // runtime.py:299-300
+  if (nops < 1) return fail(UM_EVALUE, "nops must be >= 1");  // runtime.py:91-92
   if (!out) return fail(UM_EVALUE, "null out pointer");
   *out = (ti + tj) % nops;
   return UM_OK;

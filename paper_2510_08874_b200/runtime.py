@@ -17,7 +17,7 @@ signatures.  What runs underneath is B200-native, in four modules:
 * remote C (Stationary A/B): the K1 epilogue accumulates straight into the
   owner's tile (TMA reduce-add on the same GPU, red.global.add over NVLink to
   a peer GPU) — the reference's scratch + accumulate_tile round trip
-  (runtime.py:362-373) disappears.
+  (runtime.py:152-166) disappears.
 * `replicas`: replicated C is reduced into replica 0 by K4, distributed
   over the replica owners, either after a run-level barrier or — default
   under Stationary C — per row sub-slice as soon as every replica's K1 has
@@ -67,9 +67,9 @@ def local_gemm(a, b, c, counters=None, rank: int = 0) -> None:
 def _count_reference_traffic(A, B, C, cfg: ExecConfig, sched: DirectSchedule):
     """FabricCounters exactly as the reference's run_direct would record them.
 
-    Every remote A/B tile is a whole-tile get per op (runtime.py:427-438,
+    Every remote A/B tile is a whole-tile get per op (runtime.py:219-231,
     distmatrix.py:158); every remote C update one accumulate_tile
-    (runtime.py:338-341: one message if full-width, else one per row;
+    (runtime.py:126-135 -> distmatrix.py:170-209: one message if full-width, else one per row;
     2x bytes and messages in LOCK_GET_PUT, fabric.py:225-234).  The per-rank
     totals are computed once per schedule and accumulation mode and added in
     one step per run (the host issue path stays O(1) in the op count).

@@ -258,7 +258,7 @@ def make_numeric():
 
 def make_runtime(numeric_meta):
     out = dict(numeric=numeric_meta)
-    # request orders (RunStats.a_requests / b_requests, runtime.py:447-451)
+    # request orders (RunStats.a_requests / b_requests, runtime.py:238-243)
     req = []
     for case in [(9, 12, 12, 12, "2d", "2d", "2d", 1, 1, 1, "c", False),
                  (4, 7, 9, 5, "row", "col", "2d", 1, 1, 1, "a", False),
