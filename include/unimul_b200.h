@@ -221,6 +221,13 @@ UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
  * reference's get_async + PendingCopy.wait, fabric.py:177-201,
  * runtime.py:233-236).  Falls back to um_get inside a graph capture.        */
 UM_API int um_get_ce(const um_view* src, const um_view* dst, void* stream);
+/* *ok = 1 when a um_get_ce pull from src_device into dst_device completes
+ * while a persistent kernel holds every SM of dst_device (copy engines, not
+ * SM copy kernels), measured once per pair by doing exactly that with a
+ * 0.5 s timeout.  get_engine "auto" / "ce" use flagged copy-engine pulls only
+ * where this holds (same-device 2-D copies on the test box do NOT: the
+ * driver runs them on SMs, and a K1 spinning on their flag would starve them). */
+UM_API int um_ce_probe(int32_t dst_device, int32_t src_device, int32_t* ok);
 
 /* Arrival flag of a get: write `value` to the device word `flag` in stream
  * order (after everything enqueued before it on `stream`), without using an

@@ -140,6 +140,7 @@ _SIGS = {
     "um_accumulate": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
     "um_reduce_replicas": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     "um_get_ce": (ctypes.c_int, [_P(UmView), _P(UmView), ctypes.c_void_p]),
+    "um_ce_probe": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P(ctypes.c_int32)]),
     "um_execute": (ctypes.c_int, [_P(UmRankPlan), ctypes.c_int32, _P(UmReduceStep), ctypes.c_int32, _P(UmExecCfg)]),
     "um_sync_all": (ctypes.c_int, []),
     "um_execute_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),

@@ -67,7 +67,10 @@ class ExecConfig:
                          in-kernel, pulls from other GPUs on the copy engines
                          (um_get_ce, no SMs) followed by an arrival flag
                          (um_signal) that the K1 producer waits on inside the
-                         same launch; "ce": every pull that way.
+                         same launch -- where um_ce_probe shows the driver
+                         runs such a copy without SMs, else in-kernel; "ce":
+                         every pull on the copy engines, flagged where the
+                         probe allows, else with host-side launch splitting.
       reduce_mode        K4 for replicated C: "peer" (P2P loads, reference
                          summation order), "nvls" (multimem.ld_reduce through a
                          multicast team: needs Fabric(symmetric="vmm") and the

@@ -17,6 +17,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <ctime>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -259,6 +261,101 @@ extern "C" int um_get_ce(const um_view* src, const um_view* dst, void* stream) {
     return um_get(src, dst, stream);
   }
   if (e != cudaSuccess) return fail(UM_ECUDA, std::string("cudaMemcpyBatchAsync: ") + cudaGetErrorString(e));
+  return UM_OK;
+}
+
+// Probe kernel: one CTA per SM holding the maximum shared memory (as K1's
+// persistent grid does), every CTA spinning until *flag != 0 or ~timeout_ns;
+// block 0 reports whether the flag arrived.
+__global__ void ce_probe_kernel(const volatile uint32_t* flag, uint32_t* status, uint64_t timeout_ns) {
+  extern __shared__ uint8_t pad[];
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  uint32_t v = 0;
+  for (;;) {
+    v = *flag;
+    if (v) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) break;
+    __nanosleep(1000);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *status = v ? 1u : 2u;
+    pad[0] = 0;
+  }
+}
+
+extern "C" int um_ce_probe(int32_t dst_device, int32_t src_device, int32_t* ok) {
+  // Can a pull from src_device into dst_device (um_get_ce) complete while a
+  // persistent kernel holds every SM of dst_device?  Only then may a running
+  // K1 wait for it on an arrival flag (get_engine "auto").  Answered once per
+  // device pair by running exactly that: a max-shared-memory CTA per SM
+  // spinning on a flag that the pull's stream sets after a 2-D copy the size
+  // of a staged band (the driver may use SM copy kernels for some copies, e.g.
+  // same-device 2-D copies -- then the probe times out after 0.5 s, no hang).
+  if (!ok) return fail(UM_EVALUE, "null out pointer");
+  *ok = 0;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair((int)dst_device, (int)src_device);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *ok = it->second;
+    return UM_OK;
+  }
+  DeviceGuard g(dst_device);
+  const size_t rows = 2048, row_bytes = 8192, pitch = 8192 + 512;   // 16 MiB, strided like a slice
+  void *src = nullptr, *dst = nullptr;
+  uint32_t* words = nullptr;
+  cudaStream_t s_spin = nullptr, s_copy = nullptr;
+  int result = 0;
+  int sms = 0, max_smem = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dst_device);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dst_device);
+  auto cleanup = [&]() {
+    if (s_spin) cudaStreamDestroy(s_spin);
+    if (s_copy) cudaStreamDestroy(s_copy);
+    if (words) cudaFree(words);
+    if (dst) cudaFree(dst);
+    if (src) {
+      DeviceGuard gs(src_device);
+      cudaFree(src);
+    }
+  };
+  {
+    DeviceGuard gs(src_device);
+    if (cudaMalloc(&src, rows * pitch) != cudaSuccess) {
+      cleanup();
+      return fail(UM_ECUDA, "um_ce_probe: allocation failed");
+    }
+  }
+  if (cudaMalloc(&dst, rows * pitch) != cudaSuccess || cudaMalloc(&words, 64) != cudaSuccess ||
+      cudaMemset(words, 0, 64) != cudaSuccess || cudaStreamCreateWithFlags(&s_spin, cudaStreamNonBlocking) ||
+      cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking) ||
+      cudaFuncSetAttribute(ce_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem)) {
+    cleanup();
+    cudaGetLastError();
+    return fail(UM_ECUDA, "um_ce_probe: setup failed");
+  }
+  cudaDeviceSynchronize();
+  ce_probe_kernel<<<sms, 128, max_smem, s_spin>>>(words, words + 1, 500000000ull);
+  // the pull is queued only after the spinners hold the SMs
+  struct timespec ts = {0, 20 * 1000 * 1000};
+  nanosleep(&ts, nullptr);
+  um_view sv = {src, 0, (int64_t)rows, 0, (int64_t)(row_bytes / 2), (int64_t)(pitch / 2), UM_BF16, src_device};
+  um_view dv = {dst, 0, (int64_t)rows, 0, (int64_t)(row_bytes / 2), (int64_t)(pitch / 2), UM_BF16, dst_device};
+  int rc = um_get_ce(&sv, &dv, s_copy);
+  if (rc == UM_OK) rc = um_signal(words, 1, s_copy);
+  cudaDeviceSynchronize();
+  uint32_t status = 0;
+  cudaMemcpy(&status, words + 1, 4, cudaMemcpyDeviceToHost);
+  const cudaError_t e = cudaGetLastError();
+  result = (rc == UM_OK && e == cudaSuccess && status == 1) ? 1 : 0;
+  cleanup();
+  cache[key] = result;
+  *ok = result;
   return UM_OK;
 }
 

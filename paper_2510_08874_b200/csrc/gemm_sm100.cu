@@ -1008,7 +1008,13 @@ static const Knobs& knobs() {
   static Knobs k;
   static std::once_flag once;
   std::call_once(once, [] {
+#if UM_PROFILE
+    // variants measured and rejected (cta_group::1, B multicast across pairs,
+    // 8 epilogue warps) are instantiated in the profiling build only
     k.cg = env_int("UM_GEMM_CG", 2) == 1 ? 1 : 2;
+#else
+    k.cg = 2;
+#endif
     k.nt = env_int("UM_GEMM_NT", 0);
     k.group = env_int("UM_GEMM_GROUP", GROUP_M);
     if (k.group == 0) k.group = GROUP_M;
@@ -1017,9 +1023,14 @@ static const Knobs& knobs() {
     k.cpol = env_int("UM_GEMM_CPOL", -1);
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
+#if UM_PROFILE
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
     k.pairs = env_int("UM_GEMM_PAIRS", 1);
     if (k.pairs != 2 && k.pairs != 4) k.pairs = 1;
+#else
+    k.epi_warps = 4;
+    k.pairs = 1;
+#endif
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
     k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
@@ -1649,6 +1660,7 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   args.prof = prof;
   int rc;
   const bool g = P->ngets > 0;
+#if UM_PROFILE
   if (P->CG == 1) rc = g ? launch<1, 256, 4, GET_WARPS>(args, P->device, stream) : launch<1, 256, 4, 0>(args, P->device, stream);
   else if (P->NT == 512 && P->NP == 2)
     rc = g ? launch<2, 512, 4, GET_WARPS, 2>(args, P->device, stream) : launch<2, 512, 4, 0, 2>(args, P->device, stream);
@@ -1656,10 +1668,12 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
     rc = g ? launch<2, 512, 4, GET_WARPS, 4>(args, P->device, stream) : launch<2, 512, 4, 0, 4>(args, P->device, stream);
   else if (P->NT == 512 && P->EW == 8)
     rc = g ? launch<2, 512, 8, GET_WARPS>(args, P->device, stream) : launch<2, 512, 8, 0>(args, P->device, stream);
-  else if (P->NT == 512)
-    rc = g ? launch<2, 512, 4, GET_WARPS>(args, P->device, stream) : launch<2, 512, 4, 0>(args, P->device, stream);
-  else if (P->EW == 8)
+  else if (P->EW == 8 && P->NT != 512)
     rc = g ? launch<2, 256, 8, GET_WARPS>(args, P->device, stream) : launch<2, 256, 8, 0>(args, P->device, stream);
+  else
+#endif
+  if (P->NT == 512)
+    rc = g ? launch<2, 512, 4, GET_WARPS>(args, P->device, stream) : launch<2, 512, 4, 0>(args, P->device, stream);
   else
     rc = g ? launch<2, 256, 4, GET_WARPS>(args, P->device, stream) : launch<2, 256, 4, 0>(args, P->device, stream);
   args.prof = nullptr;

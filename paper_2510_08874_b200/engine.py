@@ -143,12 +143,27 @@ class _RankRun:
         eng = self.cfg.get_engine
         shared = fab.world.size > 1 and fab.devices_shared_across_processes()
 
-        def same_gpu(j):
+        def owner_gpu(j):
+            """The owner's device index as seen here (-1: unknown, another process's GPU)."""
             d = fab.device_of(s.fetches[j].owner)
-            return d == self.dev or (d < 0 and shared)
+            return self.dev if (d < 0 and shared) else d
 
-        in_kernel = [eng == "kernel" or (eng == "auto" and same_gpu(j)) for j in range(nf)]
-        flagged = [eng in ("auto", "ce") and not in_kernel[j] for j in range(nf)]
+        def ce_ok(j):
+            # a flagged copy-engine pull is only safe where the driver runs it
+            # without SMs while K1 holds them all (um_ce_probe, measured once per
+            # device pair); another process's GPU is probed through any peer
+            src = owner_gpu(j)
+            if src < 0:
+                n = ctypes.c_int32(0)
+                _capi.check(lib.um_device_count(ctypes.byref(n)), "um_device_count")
+                src = (self.dev + 1) % max(1, n.value)
+            ok = ctypes.c_int32(0)
+            _capi.check(lib.um_ce_probe(self.dev, src, ctypes.byref(ok)), "um_ce_probe")
+            return bool(ok.value)
+
+        in_kernel = [eng == "kernel" or (eng == "auto" and (owner_gpu(j) == self.dev or not ce_ok(j)))
+                     for j in range(nf)]
+        flagged = [eng in ("auto", "ce") and not in_kernel[j] and ce_ok(j) for j in range(nf)]
         for i in range(len(s.ops)):
             for src, v in ((s.a_src[i], views[i][0]), (s.b_src[i], views[i][1])):
                 if src >= 0 and not _tma_ok(v):

@@ -104,7 +104,9 @@ def test_one_cta_variant_matches(cuda):
         "b=torch.randint(-8,9,(900,600),generator=g,device='cuda').to(torch.bfloat16);"
         "c=torch.zeros(700,600,device='cuda'); kernels.gemm_accumulate(a,b,c);"
         "assert torch.equal(c,(a.double()@b.double()).float()); print('OK')")
-    env = dict(os.environ, UM_GEMM_CG="1")
+    env = dict(os.environ, UM_GEMM_CG="1",    # a profiling-build-only variant
+               UNIMUL_B200_LIB=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "paper_2510_08874_b200", "_lib", "libunimul_b200_prof.so"))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
                          timeout=300)
@@ -178,3 +180,23 @@ def test_wait_flag_orders_op_after_copy_engine_pull(cuda):
                 "um_gemm_acc_batch")
     torch.cuda.synchronize()
     assert torch.equal(c, ref_acc(torch.zeros_like(c), a, b_host.cuda()))
+
+
+def test_ce_probe_reports_and_caches(cuda):
+    """um_ce_probe on this box: a same-device pull while a persistent grid holds
+    every SM.  Whatever the driver does, the probe returns (no hang) and the
+    answer is cached."""
+    import ctypes
+    import time
+
+    from paper_2510_08874_b200 import _capi
+
+    lib = _capi.load()
+    ok = ctypes.c_int32(-1)
+    assert lib.um_ce_probe(0, 0, ctypes.byref(ok)) == 0, _capi.last_error()
+    assert ok.value in (0, 1)
+    print(f"same-device copy-engine pull completes under a full persistent grid: {bool(ok.value)}")
+    t0 = time.perf_counter()
+    ok2 = ctypes.c_int32(-1)
+    assert lib.um_ce_probe(0, 0, ctypes.byref(ok2)) == 0 and ok2.value == ok.value
+    assert time.perf_counter() - t0 < 0.05

@@ -41,8 +41,23 @@ ops = (C.UmGemmOp * parts)(*[C.UmGemmOp(view(a, 0, m, i * kc, (i + 1) * kc, C.UM
 C.check(lib.um_gemm_acc_batch(ops, parts, 0, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), 'batch')
 torch.cuda.synchronize()
 assert torch.equal(c.double(), a.double() @ b.double())
+# a fused launch with in-kernel gets (tail split acts on these), k-chains and bands
+import numpy as np
+from paper_2510_08874_b200 import ExecConfig, execute_multiply
+from paper_2510_08874_b200.cli import build_problem
+for case in ((2048, 2048, 2048, 8, "2d", "col", "row", 1, 1, 1), (1536, 1024, 2048, 8, "2d", "2d", "2d", 2, 2, 2)):
+    fab, A, B, C_, a_, b_ = build_problem(*case, seed=71)
+    for _ in range(2):
+        C_.zero_()
+        execute_multiply(A, B, C_, ExecConfig(get_engine="kernel"))
+        assert np.array_equal(C_.gather(0), a_ @ b_), case
 print('OK')
 """
+
+PROF_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_08874_b200", "_lib",
+                        "libunimul_b200_prof.so")
+# variants measured and rejected in round 1 exist only in the profiling build
+PROF_ONLY = ("UM_GEMM_PAIRS", "UM_GEMM_EPI_WARPS", "UM_GEMM_CG", "UM_GEMM_EPI_DEBUG")
 
 
 @pytest.mark.parametrize("env", [
@@ -56,10 +71,15 @@ print('OK')
     {"UM_GEMM_CHAIN": "0"},
     {"UM_GEMM_EPI_DEBUG": "red"},                        # red.global epilogue for local C
     {"UM_GEMM_APOL": "0", "UM_GEMM_BPOL": "0", "UM_GEMM_CPOL": "1"},
-    {"UM_GEMM_TAIL_SPLIT": "1"},                         # last wave split along k (fused launches)
+    {"UM_GEMM_TAIL_SPLIT": "1"},                         # last wave split along k (fused launches, gets)
+    {"UM_GEMM_SKSTART": "0"},                            # no staggered start
+    {"UM_GEMM_CG": "1"},                                 # cta_group::1 (profiling build)
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_variant_exact(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(env)
+    if any(k in env for k in PROF_ONLY):
+        env["UNIMUL_B200_LIB"] = PROF_LIB
     out = subprocess.run([sys.executable, "-c", SCRIPT], env=dict(os.environ, **env), cwd=root,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "OK" in out.stdout, (out.stdout[-1000:], out.stderr[-2000:])
