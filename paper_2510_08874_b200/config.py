@@ -63,14 +63,21 @@ class ExecConfig:
                          with the gets overlapping the GEMMs of earlier ops;
                          "copy": copy-engine pulls on a get stream, the host
                          splits K1 launches at every pull not yet waited on;
-                         "auto" (default): pulls from the caller's own GPU
-                         in-kernel, pulls from other GPUs on the copy engines
-                         (um_get_ce, no SMs) followed by an arrival flag
-                         (um_signal) that the K1 producer waits on inside the
-                         same launch -- where um_ce_probe shows the driver
-                         runs such a copy without SMs, else in-kernel; "ce":
-                         every pull on the copy engines, flagged where the
-                         probe allows, else with host-side launch splitting.
+                         "auto": pulls from the caller's own GPU in-kernel,
+                         pulls from other GPUs on the copy engines (um_get_ce,
+                         no SMs) followed by an arrival flag (um_signal) that
+                         the K1 producer waits on inside the same launch --
+                         where um_ce_probe shows the driver runs such a copy
+                         without SMs, else in-kernel; the launch leaves two
+                         CTA pairs' SMs free so an SM-run copy still
+                         progresses.  "ce": every pull that way (a protocol
+                         test mode: with several ranks co-resident on ONE
+                         GPU, full-size same-device pulls deadlocked the
+                         spinning K1s on the test box).  The default stays
+                         "kernel" (deadlock-free by construction: every pull
+                         is done by warps of the same launch) until the
+                         cross-GPU copy-engine path is validated on a
+                         multi-GPU box.
       reduce_mode        K4 for replicated C: "peer" (P2P loads, reference
                          summation order), "nvls" (multimem.ld_reduce through a
                          multicast team: needs Fabric(symmetric="vmm") and the
@@ -90,7 +97,7 @@ class ExecConfig:
     gemm_batch: int = 0
     fused_accumulate: bool = True
     reduce_distributed: bool = True
-    get_engine: str = "auto"
+    get_engine: str = "kernel"
     mn_split: int = 4
     overlap_reduce: bool = True
     chain_order: bool = True

@@ -306,7 +306,9 @@ extern "C" int um_ce_probe(int32_t dst_device, int32_t src_device, int32_t* ok) 
     return UM_OK;
   }
   DeviceGuard g(dst_device);
-  const size_t rows = 2048, row_bytes = 8192, pitch = 8192 + 512;   // 16 MiB, strided like a slice
+  // a strided slice (2048 rows of 8 KiB) and a contiguous 64 MiB block: both
+  // shapes the staging pulls take
+  const size_t rows = 8192, row_bytes = 8192, pitch = 8192;
   void *src = nullptr, *dst = nullptr;
   uint32_t* words = nullptr;
   cudaStream_t s_spin = nullptr, s_copy = nullptr;
@@ -346,7 +348,10 @@ extern "C" int um_ce_probe(int32_t dst_device, int32_t src_device, int32_t* ok) 
   nanosleep(&ts, nullptr);
   um_view sv = {src, 0, (int64_t)rows, 0, (int64_t)(row_bytes / 2), (int64_t)(pitch / 2), UM_BF16, src_device};
   um_view dv = {dst, 0, (int64_t)rows, 0, (int64_t)(row_bytes / 2), (int64_t)(pitch / 2), UM_BF16, dst_device};
+  um_view ss = {src, 0, 2048, 0, 4096 - 256, 4096, UM_BF16, src_device};
+  um_view ds = {dst, 0, 2048, 0, 4096 - 256, 4096, UM_BF16, dst_device};
   int rc = um_get_ce(&sv, &dv, s_copy);
+  if (rc == UM_OK) rc = um_get_ce(&ss, &ds, s_copy);
   if (rc == UM_OK) rc = um_signal(words, 1, s_copy);
   cudaDeviceSynchronize();
   uint32_t status = 0;

@@ -249,6 +249,7 @@ struct alignas(64) LaunchArgs {
   int nslots;
   int nstag;                  // staggered start: the first nstag tiles run a k-prefix, their rest comes last
   int stag_ok;                // host: this launch may use a staggered start (set at prepare)
+  int ext_waits;              // host: some op waits on an external arrival flag (copy-engine pull)
   uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
   unsigned long long* prof;   // (profiling, UM_GEMM_STALLS) per cluster: MMA-thread cycles total / waiting
                               // for operands / for the epilogue to free TMEM / for the next tile
@@ -1090,6 +1091,11 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   // their launches (and the pulls inside them) run side by side
   const int cap = grid_limit(device);
   if (cap > 0) units = std::max(1, std::min(units, cap));
+  // ops waiting on external arrival flags (copy-engine pulls): keep two CTA
+  // pairs' SMs free, so the transfer always makes progress even where the
+  // driver runs a copy on SMs rather than copy engines (a persistent grid
+  // holding every SM would starve it: observed for same-device copies)
+  if (args.ext_waits) units = std::max(1, std::min(units, sms / CG - 2));
   if (NP > 1) units = std::max(NP, units - units % NP);   // the grid must divide into big clusters
   static int occ[64] = {0};
   static const bool fixed = getenv("UM_GEMM_PAIRS_FIXED") && atoi(getenv("UM_GEMM_PAIRS_FIXED")) == 1;
@@ -1554,6 +1560,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   args.nwork = (int)works.size();
   args.total_tiles = total;
   args.nslots = (int)slot_flags.size();
+  args.ext_waits = 0;
+  for (const Work& w : works) args.ext_waits |= w.wait_flag != nullptr;
   // staggered start (unit_span): plain launches only -- no in-kernel gets, no
   // completion slots (a split tile is written twice), no k-chains, and tiles
   // long enough (>= 8 k-blocks) that a prefix/remainder pair stays mainloop-bound

@@ -12,48 +12,68 @@ K4), so results are identical to execute_multiply.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
-from paper_2510_08874_b200.trace import nvtx
+from paper_2510_08874_b200 import _capi
 from paper_2510_08874_b200 import runtime as rt
 from paper_2510_08874_b200.errors import ContractError
+from paper_2510_08874_b200.fabric import um_dtype
 from paper_2510_08874_b200.opgen import LocalMatMulOp
 from paper_2510_08874_b200.tiling import Bounds2D, Range
+from paper_2510_08874_b200.trace import nvtx
 
 
-def _restrict(op: LocalMatMulOp, r0: int, r1: int) -> LocalMatMulOp | None:
+def _restrict(op: LocalMatMulOp, r0: int, r1: int, c0: int | None = None, c1: int | None = None
+              ) -> LocalMatMulOp | None:
+    """The part of `op` inside global C rows [r0, r1) (and columns [c0, c1))."""
     lo, hi = max(op.m_bound.lo, r0), min(op.m_bound.hi, r1)
     if hi <= lo:
         return None
+    nlo, nhi = op.n_bound.lo, op.n_bound.hi
+    if c0 is not None:
+        nlo, nhi = max(nlo, c0), min(nhi, c1)
+        if nhi <= nlo:
+            return None
     da, db = lo - op.m_bound.lo, hi - op.m_bound.lo
+    ea, eb = nlo - op.n_bound.lo, nhi - op.n_bound.lo
     return LocalMatMulOp(
-        op.a_tile, op.b_tile, op.c_tile, Range(lo, hi), op.k_bound, op.n_bound,
+        op.a_tile, op.b_tile, op.c_tile, Range(lo, hi), op.k_bound, Range(nlo, nhi),
         Bounds2D(Range(op.a_local.rows.lo + da, op.a_local.rows.lo + db), op.a_local.cols),
-        op.b_local,
-        Bounds2D(Range(op.c_local.rows.lo + da, op.c_local.rows.lo + db), op.c_local.cols))
+        Bounds2D(op.b_local.rows, Range(op.b_local.cols.lo + ea, op.b_local.cols.lo + eb)),
+        Bounds2D(Range(op.c_local.rows.lo + da, op.c_local.rows.lo + db),
+                 Range(op.c_local.cols.lo + ea, op.c_local.cols.lo + eb)))
 
 
-def _copy_rows(M, host: torch.Tensor, r0: int, r1: int, stream_of, to_device: bool, events: dict):
-    """Copy the global rows [r0, r1) of every locally hosted tile of M (all replicas)."""
+def _copy_rows(M, host: torch.Tensor, r0: int, r1: int, stream_of, to_device: bool, events: dict,
+               c0: int = 0, c1: int | None = None):
+    """Copy the global block rows [r0, r1) x columns [c0, c1) of every locally
+    hosted tile of M (all replicas up; replica 0 down)."""
     fab = M.fabric
+    if c1 is None:
+        c1 = M.global_shape.cols
     for (rep, t), seg in M._segments.items():
         if seg.storage is None or seg.length == 0:
             continue
         b = M.tile_bounds(t)
         lo, hi = max(r0, b.rows.lo), min(r1, b.rows.hi)
-        if hi <= lo:
+        clo, chi = max(c0, b.cols.lo), min(c1, b.cols.hi)
+        if hi <= lo or chi <= clo:
             continue
         if not to_device and rep != 0:
             continue
         dev = seg.device
         s = stream_of(dev)
-        view = seg.view2d()[lo - b.rows.lo:hi - b.rows.lo]
-        hslice = host[lo:hi, b.cols.lo:b.cols.hi]
-        with torch.cuda.stream(s):
-            if to_device:
-                view.copy_(hslice, non_blocking=True)
-            else:
-                hslice.copy_(view, non_blocking=True)
+        # one strided 2-D copy engine transfer (cudaMemcpy2DAsync via um_get)
+        # between the pinned host block and the tile's block: no host-side
+        # staging for column blocks
+        dv = seg.um_view(lo - b.rows.lo, hi - b.rows.lo, clo - b.cols.lo, chi - b.cols.lo)
+        hv = _capi.UmView(host.data_ptr(), lo, hi, clo, chi, host.stride(0), um_dtype(host.dtype), -1)
+        src, dst = (hv, dv) if to_device else (dv, hv)
+        with torch.cuda.device(dev):
+            _capi.check(_capi.load().um_get(ctypes.byref(src), ctypes.byref(dst), ctypes.c_void_p(s.cuda_stream)),
+                        "um_get")
         ev = torch.cuda.Event()
         ev.record(s)
         events.setdefault(dev, []).append(ev)
@@ -61,14 +81,50 @@ def _copy_rows(M, host: torch.Tensor, r0: int, r1: int, stream_of, to_device: bo
 
 
 @nvtx("um:multiply_from_host")
+def _check_host(*ts):
+    for t in ts:
+        if t.device.type != "cpu" or t.dim() != 2 or t.stride(1) != 1:
+            raise ContractError("host buffers must be 2-D CPU tensors with unit column stride (pinned for overlap)")
+
+
+def _shell_order(P: int, Q: int) -> list:
+    """Blocks (i, j) of a P x Q grid in growing 'shells' max(i/P, j/Q): every
+    shell needs one more row panel of A and one more column panel of B, so
+    the uploads are spread over the run and the first block (and with it the
+    first download) starts after 1/P of A and 1/Q of B instead of all of B."""
+    return sorted(((i, j) for i in range(P) for j in range(Q)),
+                  key=lambda ij: (max((ij[0] + 1) / P, (ij[1] + 1) / Q), ij[0], ij[1]))
+
+
 def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_out: torch.Tensor,
-                       cfg: rt.ExecConfig | None = None, panels: int = 8, copy_streams: int = 1) -> dict:
+                       cfg: rt.ExecConfig | None = None, panels: int = 8, copy_streams: int = 1,
+                       col_panels: int | None = None) -> dict:
     """C += A @ B with A, B uploaded from host and replica 0 of C downloaded to c_out.
 
     a_host: (m, k) host tensor in A's dtype; b_host: (k, n) in B's dtype;
     c_out: (m, n) float32 host tensor.  Pinned memory makes all three copies
     asynchronous.  Returns {rank: RunStats} summed over panels.
+
+    col_panels (Q): > 1 cuts C into panels x Q blocks run in shell order
+    (_shell_order) with B uploaded by column panels as the blocks need them;
+    None picks a 4 x 4 block grid when B is at least a quarter of A's bytes
+    and C is not replicated (cfg5-like squares, where uploading all of B
+    first leaves the download direction idle for B's whole transfer), else
+    row panels (Q = 1, B uploaded whole first).  Measured at cfg5 p = 1 on
+    one B200 (tools/e2e_probe.py): 32 x 1 row panels 34.3 ms per step, 4 x 4
+    blocks 31.3, 16 x 4 31.6, 8 x 8 33.4 (host issue per block adds up).
     """
+    _check_host(a_host, b_host, c_out)
+    if col_panels is None:
+        big_b = B.global_shape.rows * B.global_shape.cols * 4 >= A.global_shape.rows * A.global_shape.cols
+        if big_b and C.c == 1:
+            panels, col_panels = 4, 4
+        else:
+            col_panels = 1
+    if col_panels > 1:
+        if C.c > 1:
+            raise ContractError("column panels need unreplicated C (the replica reduction runs per row window)")
+        return _multiply_blocks(A, B, C, a_host, b_host, c_out, cfg, panels, col_panels, copy_streams)
     cfg = cfg or rt.ExecConfig()
     rt._check_operands(A, B, C)
     m, k = A.global_shape.rows, A.global_shape.cols
@@ -139,6 +195,86 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
                 d2h_s[d][i % nst].wait_event(ev)
         down: dict = {}
         _copy_rows(C, c_out, r0, r1, lambda d: d2h_s[d][i % nst], False, down)
+        done_all += [e for evs in down.values() for e in evs] + done
+    rt._join_current(fab, done_all)
+    for r, st in results.items():
+        st.flops = int(fab.counters.flops[r])
+    return results
+
+
+@nvtx("um:multiply_from_host_blocks")
+def _multiply_blocks(A, B, C, a_host, b_host, c_out, cfg, P: int, Q: int, copy_streams: int) -> dict:
+    """multiply_from_host over a P x Q block grid of C in shell order."""
+    cfg = cfg or rt.ExecConfig()
+    rt._check_operands(A, B, C)
+    m, k = A.global_shape.rows, A.global_shape.cols
+    n = B.global_shape.cols
+    if tuple(a_host.shape) != (m, k) or tuple(b_host.shape) != (k, n) or tuple(c_out.shape) != (m, n):
+        raise ContractError("host buffers must match the global shapes of A, B and C")
+    fab = A.fabric
+    fab.heap.exchange()
+    devs = sorted({fab.device_of(r) for r in fab.local_ranks()})
+    nst = max(1, copy_streams)
+    h2d_s = {d: [_side_stream(fab, d, f"h2d{i}") for i in range(nst)] for d in devs}
+    d2h_s = {d: [_side_stream(fab, d, f"d2h{i}") for i in range(nst)] for d in devs}
+    start = rt._current_events(fab)
+    for d in devs:
+        for ev in start:
+            for st_ in h2d_s[d] + d2h_s[d]:
+                st_.wait_event(ev)
+    full_ops = {r: rt.rotated_ops(A, B, C, cfg, r) for r in fab.local_ranks()}
+    cross = rt._cross_process(A, B, C, cfg)
+    results = {r: rt.RunStats() for r in fab.local_ranks()}
+    rb = [m * i // P for i in range(P + 1)]
+    cb = [n * j // Q for j in range(Q + 1)]
+    a_ev: dict = {}
+    b_ev: dict = {}
+    done_all = []
+    for step, (i, j) in enumerate(_shell_order(P, Q)):
+        r0, r1, c0, c1 = rb[i], rb[i + 1], cb[j], cb[j + 1]
+        if r1 <= r0 or c1 <= c0:
+            continue
+        if i not in a_ev:                     # A row panel i, the first time a block needs it
+            up: dict = {}
+            _copy_rows(A, a_host, r0, r1, lambda d: h2d_s[d][0], True, up)
+            a_ev[i] = [e for evs in up.values() for e in evs]
+        if j not in b_ev:                     # B column panel j
+            up = {}
+            _copy_rows(B, b_host, 0, k, lambda d: h2d_s[d][0], True, up, c0, c1)
+            b_ev[j] = [e for evs in up.values() for e in evs]
+        ready = a_ev[i] + b_ev[j]
+        if cross:
+            fab.synchronize()
+        runs = []
+        for r in fab.local_ranks():
+            ops = [o for o in (_restrict(op, r0, r1, c0, c1) for op in full_ops[r]) if o is not None]
+            if not ops:
+                continue
+            pkey = ("block", cfg.stationarity, cfg.staging, cfg.same_device_gets, r, r0, r1, c0, c1)
+            cache = rt.schedule_cache(A, B, C)
+            sched = cache.get(pkey)
+            if sched is None:
+                sched = cache[pkey] = rt.lower_direct(A, B, C, cfg, r, ops=ops)
+            rt._count_reference_traffic(A, B, C, cfg, sched)
+            runs.append(rt._RankRun(A, B, C, cfg, sched, ready).issue())
+        done = [run.done for run in runs]
+        for run in runs:
+            st = results[run.caller]
+            st.executed_ops += run.stats.executed_ops
+            st.device_order += run.stats.device_order
+            st.a_requests += run.stats.a_requests
+            st.b_requests += run.stats.b_requests
+            st.launches += run.stats.launches
+            st.gets += run.stats.gets
+            st.staged_bytes += run.stats.staged_bytes
+        if cross:
+            fab.synchronize()
+        s_down = step % nst
+        for d in devs:
+            for ev in done:
+                d2h_s[d][s_down].wait_event(ev)
+        down: dict = {}
+        _copy_rows(C, c_out, r0, r1, lambda d: d2h_s[d][s_down], False, down, c0, c1)
         done_all += [e for evs in down.values() for e in evs] + done
     rt._join_current(fab, done_all)
     for r, st in results.items():
