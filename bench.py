@@ -503,8 +503,20 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     h2d = nbytes(A) + nbytes(B)
     d2h = nbytes(C, replica0_only=True)
 
-    def step():
-        multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, copy_streams=args.copy_streams)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1 and args.e2e_graph:
+        # the host-streaming multiply replayed as one CUDA graph: every replay
+        # still uploads A and B from the pinned host buffers and downloads C
+        from paper_2510_08874_b200.hostio import CapturedHostMultiply
+
+        cap = CapturedHostMultiply(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, col_panels=args.col_panels)
+
+        def step():
+            cap.replay()
+    else:
+        def step():
+            multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, copy_streams=args.copy_streams,
+                               col_panels=args.col_panels)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -523,8 +535,10 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     bw = pcie_bandwidth(dev)
     floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "api": "hostio.multiply_from_host",
-            "panels": args.panels, "copy_streams": args.copy_streams,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "api": ("hostio.multiply_from_host" if (world > 1 or not args.e2e_graph)
+                    else "hostio.CapturedHostMultiply (multiply_from_host as one CUDA graph)"),
+            "panels": args.panels, "col_panels": args.col_panels, "copy_streams": args.copy_streams,
             "roofline": {"bound": "pcie", "floor_ms_per_step": floor_ms, "frac": floor_ms / ms, **bw}}
 
 
@@ -570,7 +584,13 @@ def main():
     ap.add_argument("--oversubscribe", action="store_true",
                     help="allow more ranks than visible GPUs (ranks time-share a GPU; functional runs only)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--panels", type=int, default=32, help="row panels of the host-streaming e2e path")
+    ap.add_argument("--panels", type=int, default=4,
+                    help="row panels of the host-streaming e2e path (cfg5: a panels x panels block grid; "
+                         "measured 4 x 4 30 ms, 8 x 8 32 ms, 16 x 16 38 ms per step, profiles/r2_e2e_grid.log)")
+    ap.add_argument("--col-panels", type=int, default=None,
+                    help="column panels of the e2e block grid (default: hostio's choice)")
+    ap.add_argument("--e2e-graph", action="store_true",
+                    help="e2e through hostio.CapturedHostMultiply (the same copies + launches replayed as a CUDA graph)")
     ap.add_argument("--copy-streams", type=int, default=1, help="copy streams per direction in the e2e path (measured: 1 best)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")

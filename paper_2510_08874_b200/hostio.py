@@ -107,20 +107,18 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
 
     col_panels (Q): > 1 cuts C into panels x Q blocks run in shell order
     (_shell_order) with B uploaded by column panels as the blocks need them;
-    None picks a 4 x 4 block grid when B is at least a quarter of A's bytes
-    and C is not replicated (cfg5-like squares, where uploading all of B
-    first leaves the download direction idle for B's whole transfer), else
-    row panels (Q = 1, B uploaded whole first).  Measured at cfg5 p = 1 on
-    one B200 (tools/e2e_probe.py): 32 x 1 row panels 34.3 ms per step, 4 x 4
-    blocks 31.3, 16 x 4 31.6, 8 x 8 33.4 (host issue per block adds up).
+    None picks a panels x panels block grid when B is at least a quarter of
+    A's bytes and C is not replicated (cfg5-like squares, where uploading all
+    of B first leaves the download direction idle for B's whole transfer),
+    else row panels (Q = 1, B uploaded whole first).  Measured at cfg5 p = 1
+    on one B200 (tools/e2e_probe.py), eager issue: 32 x 1 row panels 34.3 ms
+    per step, 4 x 4 blocks 31.3, 8 x 8 33.4 (host-bound: the issue of 64
+    blocks); CapturedHostMultiply removes the host cost of fine grids.
     """
     _check_host(a_host, b_host, c_out)
     if col_panels is None:
         big_b = B.global_shape.rows * B.global_shape.cols * 4 >= A.global_shape.rows * A.global_shape.cols
-        if big_b and C.c == 1:
-            panels, col_panels = 4, 4
-        else:
-            col_panels = 1
+        col_panels = panels if (big_b and C.c == 1) else 1
     if col_panels > 1:
         if C.c > 1:
             raise ContractError("column panels need unreplicated C (the replica reduction runs per row window)")
@@ -289,3 +287,57 @@ def _side_stream(fab, dev: int, kind: str) -> torch.cuda.Stream:
         s = torch.cuda.Stream(device=dev)
         fab._streams[key] = s
     return s
+
+
+def _sub_counters(a, b):
+    a.bytes -= b.bytes
+    a.msgs -= b.msgs
+    a.wire_bytes -= b.wire_bytes
+    a.flops -= b.flops
+
+
+class CapturedHostMultiply:
+    """multiply_from_host recorded once into a CUDA graph and replayed.
+
+    Every replay is one complete end-to-end multiply: the H2D copies of A
+    and B from the caller's pinned host buffers, every rank's K1 launches
+    (with their pulls), and the D2H copy of C -- the same device work as
+    multiply_from_host, without the host issue cost that dominates fine
+    block grids (cfg5 at 8 x 8 blocks: ~0.5 ms of Python per block, i.e. a
+    host-bound 33 ms step).  The buffers are fixed at capture: refill
+    a_host / b_host in place between replays, read c_out after the replay's
+    stream work.  Single process; unreplicated C for block grids (as
+    multiply_from_host).
+    """
+
+    def __init__(self, A, B, C, a_host, b_host, c_out, cfg: rt.ExecConfig | None = None, panels: int = 8,
+                 col_panels: int | None = None, warmup: int = 1):
+        fab = A.fabric
+        if fab.world.size != 1:
+            raise ContractError("CapturedHostMultiply is single-process")
+        cfg = cfg or rt.ExecConfig()
+        self.args = (A, B, C, a_host, b_host, c_out, cfg, panels, col_panels)
+        for _ in range(max(1, warmup)):       # builds schedules, plans, staging pools and streams
+            multiply_from_host(A, B, C, a_host, b_host, c_out, cfg, panels=panels, col_panels=col_panels)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        before = fab.counters.__class__(fab.counters.nprocs)
+        before.merge(fab.counters)
+        with torch.cuda.graph(self.graph, stream=side):
+            self.stats = multiply_from_host(A, B, C, a_host, b_host, c_out, cfg, panels=panels,
+                                            col_panels=col_panels)
+        # the capture counted one multiply on the host but executed nothing: keep
+        # that as the per-replay delta and take it back out of the counters
+        self.delta = fab.counters.__class__(fab.counters.nprocs)
+        self.delta.merge(fab.counters)
+        _sub_counters(self.delta, before)
+        _sub_counters(fab.counters, self.delta)
+        self._pinned = rt.schedule_cache(A, B, C)      # the graph replays these plans' buffers
+
+    def replay(self) -> dict:
+        """One more end-to-end C += A @ B (stream-ordered on the current stream)."""
+        self.graph.replay()
+        self.args[0].fabric.counters.merge(self.delta)
+        return self.stats
