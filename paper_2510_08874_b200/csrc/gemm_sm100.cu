@@ -183,8 +183,20 @@ __device__ __forceinline__ void tile_coords(const Work& wk, int lt, int& mb, int
 // the last wave (list scheduling then ends within one k-block-sized piece of
 // the ideal T / pairs).  Both pieces reduce-add into C (atomic), so they need
 // no ordering.  Returns the tile index; [kb0, kb1) is the unit's k range.
-__device__ __forceinline__ int unit_span(const Work* works, int nwork, int total_tiles, int nstag, int u, int& w,
-                                         int& kb0, int& kb1) {
+//
+// Split-k (`nsplit` > 1, launches with fewer tiles than CTA pairs): unit u is
+// piece u / total_tiles of tile u % total_tiles, the pieces cutting the tile's
+// k-blocks evenly, so a small launch spreads over nsplit x more SMs.
+__device__ __forceinline__ int unit_span(const Work* works, int nwork, int total_tiles, int nstag, int nsplit, int u,
+                                         int& w, int& kb0, int& kb1) {
+  if (nsplit > 1) {
+    const int t = u % total_tiles, piece = u / total_tiles;
+    w = find_work(works, nwork, t);
+    const int kb = works[w].num_kb;
+    kb0 = (int)(((long long)piece * kb) / nsplit);
+    kb1 = (int)(((long long)(piece + 1) * kb) / nsplit);
+    return t;
+  }
   const int t = u >= total_tiles ? u - total_tiles : u;
   w = find_work(works, nwork, t);
   const int kb = works[w].num_kb;
@@ -250,6 +262,7 @@ struct alignas(64) LaunchArgs {
   int nstag;                  // staggered start: the first nstag tiles run a k-prefix, their rest comes last
   int stag_ok;                // host: this launch may use a staggered start (set at prepare)
   int ext_waits;              // host: some op waits on an external arrival flag (copy-engine pull)
+  int nsplit;                 // split-k pieces per tile (small launches), 1 = off
   uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
   unsigned long long* prof;   // (profiling, UM_GEMM_STALLS) per cluster: MMA-thread cycles total / waiting
                               // for operands / for the epilogue to free TMEM / for the next tile
@@ -276,7 +289,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   const int nwork = args.nwork;
   const int total_tiles = args.total_tiles;
   const int nstag = args.nstag;
-  const int total_units = total_tiles + nstag;   // work units handed out by the tile scheduler
+  const int nsplit = args.nsplit;
+  // work units handed out by the tile scheduler
+  const int total_units = nsplit > 1 ? total_tiles * nsplit : total_tiles + nstag;
   int* const tile_counter = args.counters;       // [0] next tile, [1] finished clusters
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -449,7 +464,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           break;
         }
         int w0, ukb0, ukb1;
-        t = unit_span(works, nwork, total_tiles, nstag, t, w0, ukb0, ukb1);
+        t = unit_span(works, nwork, total_tiles, nstag, nsplit, t, w0, ukb0, ukb1);
         int mb, nb;
         tile_coords(works[w0], t - works[w0].tile_start, mb, nb);
         // a k-chain: the segments (ops with the same C region) are loaded one
@@ -487,9 +502,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, wk.b_row0 + kb * BK);
         };
         const int pf = wk.prefetch;
-        // k-blocks of this segment; a staggered unit (single-segment works only)
-        // covers [ukb0, ukb1) of its tile
-        const int kbs = nstag ? ukb0 : 0, kbe = nstag ? ukb1 : wk.seg_kb;
+        // k-blocks of this segment; a staggered or split-k unit (single-segment
+        // works only) covers [ukb0, ukb1) of its tile
+        const bool piece = nstag > 0 || nsplit > 1;
+        const int kbs = piece ? ukb0 : 0, kbe = piece ? ukb1 : wk.seg_kb;
         for (int kb = kbs; kb < min(kbs + pf, kbe); ++kb) prefetch(kb);
         for (int kb = kbs; kb < kbe; ++kb) {
           if (pf > 0 && kb + pf < kbe) prefetch(kb + pf);
@@ -597,7 +613,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
 #endif
         int w, ukb0, ukb1;
-        t = unit_span(works, nwork, total_tiles, nstag, t, w, ukb0, ukb1);
+        t = unit_span(works, nwork, total_tiles, nstag, nsplit, t, w, ukb0, ukb1);
         const int num_kb = ukb1 - ukb0;    // k-blocks of this unit (the whole chain's, unstaggered)
         const int buf = it % C::NBUF;
         const uint32_t tph = (uint32_t)(it / C::NBUF) & 1u;
@@ -695,7 +711,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       decode(__shfl_sync(0xffffffffu, t, 0), t, row_off);
       if (t >= total_units) break;
       int w, ukb0_unused, ukb1_unused;
-      t = unit_span(works, nwork, total_tiles, nstag, t, w, ukb0_unused, ukb1_unused);
+      t = unit_span(works, nwork, total_tiles, nstag, nsplit, t, w, ukb0_unused, ukb1_unused);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
       if (wk.c_pol >= 0) cpol = cpols[wk.c_pol];
@@ -1004,6 +1020,7 @@ struct Knobs {
   int cpf = 0;
   int stagger = 0;
   int skstart = 1;
+  int splitk = 1;
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -1038,6 +1055,7 @@ static const Knobs& knobs() {
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
     k.skstart = env_int("UM_GEMM_SKSTART", 1) ? 1 : 0;
+    k.splitk = env_int("UM_GEMM_SPLITK", 1) ? 1 : 0;
   });
   return k;
 }
@@ -1128,7 +1146,23 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   {
     const int waves = (total_tiles + units - 1) / max(1, units);
     const double idle = waves > 0 ? 1.0 - (double)total_tiles / ((double)waves * units) : 0.0;
-    args.nstag = (NP == 1 && args.stag_ok && total_tiles > units && idle > 0.10) ? units : 0;
+    args.nstag = (NP == 1 && args.stag_ok && !args.ext_waits && total_tiles > units && idle > 0.10) ? units : 0;
+  }
+  // split-k for launches with fewer tiles than pairs: each piece keeps >= 4
+  // k-blocks (its mainloop then still covers the pipeline fill); the grid
+  // grows to the pieces
+  args.nsplit = 1;
+  if (NP == 1 && args.stag_ok && !args.ext_waits && knobs().splitk && total_tiles < sms / CG) {
+    int min_kb = 1 << 30;
+    const Work* ws = args.works ? nullptr : args.inl_works;
+    if (ws) for (int i = 0; i < args.nwork; ++i) min_kb = std::min(min_kb, ws[i].num_kb);
+    const int s = ws ? std::min((sms / CG) / std::max(1, total_tiles), min_kb / 4) : 1;
+    if (s >= 2) {
+      args.nsplit = s;
+      args.nstag = 0;
+      units = std::min(sms / CG, total_tiles * s);
+      if (cap > 0) units = std::max(1, std::min(units, cap));
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG, 1, 1);
@@ -1618,7 +1652,11 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   // are signalled at kernel start)
   P->empty = total == 0 && ngets == 0 && args.nslots == 0;
   void* dbuf = nullptr;
-  if (works.size() <= (size_t)MAX_INLINE_OPS) {
+  // UM_GEMM_MAPS_GLOBAL=1 (A/B knob): work list + tensor maps in a global
+  // buffer even for short lists (tests whether the first TMA's descriptor
+  // fetch from the parameter bank delays small launches)
+  static const bool maps_global = env_int("UM_GEMM_MAPS_GLOBAL", 0) != 0;
+  if (works.size() <= (size_t)MAX_INLINE_OPS && !maps_global) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
     memcpy(args.inl_works, works.data(), works.size() * sizeof(Work));
   } else {
