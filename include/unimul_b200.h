@@ -215,11 +215,11 @@ UM_API int um_gemm_config(int32_t* bm, int32_t* bn, int32_t* bk, int32_t* stages
  * copy engines of the launching stream's device (the paper's transport,
  * PAPER.md:69).                                                            */
 UM_API int um_get(const um_view* src, const um_view* dst, void* stream);
-/* The same pull requesting the copy engines (cudaMemcpyBatchAsync with
- * cudaMemcpyFlagPreferOverlapWithCompute): the SM-free transport for pulls a
+/* The same pull as one plain copy (2-D, or 1-D for a contiguous slice) that
+ * the driver runs on the copy engines for peer sources: the SM-free transport for pulls a
  * running K1 waits for through um_signal / um_gemm_op.wait_flag (the
  * reference's get_async + PendingCopy.wait, fabric.py:177-201,
- * runtime.py:233-236).  Falls back to um_get inside a graph capture.        */
+ * runtime.py:233-236).  Only used where um_ce_probe holds for the pair.     */
 UM_API int um_get_ce(const um_view* src, const um_view* dst, void* stream);
 /* *ok = 1 when a um_get_ce pull from src_device into dst_device completes
  * while a persistent kernel holds every SM of dst_device (copy engines, not

@@ -225,10 +225,11 @@ extern "C" int um_get(const um_view* src, const um_view* dst, void* stream) {
 }
 
 extern "C" int um_get_ce(const um_view* src, const um_view* dst, void* stream) {
-  // The same pull, asking the driver for the copy engines explicitly
-  // (cudaMemcpyBatchAsync + cudaMemcpyFlagPreferOverlapWithCompute, one entry
-  // per row, or one for a contiguous slice): a K1 launch that spins on the
-  // pull's arrival flag holds every SM, so the copy must not need one.
+  // The pull a running K1 waits for on an arrival flag.  A K1 launch that
+  // spins on the flag holds every SM, so the copy must not need one: one
+  // cudaMemcpy2DAsync (or cudaMemcpyAsync for a contiguous slice) that the
+  // driver runs on the copy engines for peer/IPC sources.  Whether it does is
+  // not promised by the API, so callers gate it on um_ce_probe for the pair.
   int rc;
   if ((rc = check_view(src, "src", false)) || (rc = check_view(dst, "dst", false))) return rc;
   if (src->dtype != dst->dtype) return fail(UM_ECONTRACT, "get: dtype mismatch");
@@ -237,30 +238,12 @@ extern "C" int um_get_ce(const um_view* src, const um_view* dst, void* stream) {
   const int64_t es = esize(src->dtype);
   const int64_t rows = view_rows(*src), cols = view_cols(*src);
   if (rows == 0 || cols == 0) return UM_OK;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  UM_CUDA_CHECK(cudaStreamIsCapturing(st, &cap));
-  if (cap != cudaStreamCaptureStatusNone) return um_get(src, dst, stream);   // graphs: a memcpy node
-  char* s = const_cast<char*>(static_cast<const char*>(src->base)) + (src->row_lo * src->pitch + src->col_lo) * es;
-  char* d = static_cast<char*>(dst->base) + (dst->row_lo * dst->pitch + dst->col_lo) * es;
   const bool contiguous = src->pitch == cols && dst->pitch == cols;
-  const size_t n = contiguous ? 1 : (size_t)rows;
-  std::vector<void*> srcs(n), dsts(n);
-  std::vector<size_t> sizes(n, contiguous ? (size_t)(rows * cols * es) : (size_t)(cols * es));
-  for (size_t i = 0; i < n; ++i) {
-    srcs[i] = s + i * src->pitch * es;
-    dsts[i] = d + i * dst->pitch * es;
-  }
-  cudaMemcpyAttributes attr = {};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t idx = 0, fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &idx, 1, &fail_idx, st);
-  if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
-    cudaGetLastError();
-    return um_get(src, dst, stream);
-  }
-  if (e != cudaSuccess) return fail(UM_ECUDA, std::string("cudaMemcpyBatchAsync: ") + cudaGetErrorString(e));
+  if (!contiguous) return um_get(src, dst, stream);
+  const char* s = static_cast<const char*>(src->base) + (src->row_lo * src->pitch + src->col_lo) * es;
+  char* d = static_cast<char*>(dst->base) + (dst->row_lo * dst->pitch + dst->col_lo) * es;
+  UM_CUDA_CHECK(cudaMemcpyAsync(d, s, (size_t)(rows * cols * es), cudaMemcpyDefault,
+                                reinterpret_cast<cudaStream_t>(stream)));
   return UM_OK;
 }
 
