@@ -99,7 +99,11 @@ struct Cfg {
   static constexpr int B_BYTES = B_SUBS * SUB_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = EW * EPI_BOXES * EPI_BOX_BYTES;
+#if defined(UM_PROFILE) && UM_PROFILE
+  static constexpr int BAR_BYTES = 512;   // + per-stage issue timestamps
+#else
   static constexpr int BAR_BYTES = 256;
+#endif
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static constexpr uint32_t TMEM_COLS = 512;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -126,7 +130,8 @@ struct alignas(16) Work {
   uint64_t wait_mask;         // bit i: wait until in-kernel get i has fully landed
   int32_t a_fine, b_fine;     // 1-based get whose chunks A (per tile rows) / B (per k-block rows) wait for
   int32_t c_prefetch, stagger;  // C L2 prefetch distance (k-blocks); accumulator stagger depth (0 = STAGES-1)
-  int32_t debug_halfb, pad3_;   // profiling only: skip half of the B loads (wrong results)
+  int32_t debug_halfb;          // profiling only: skip half of the B loads (wrong results)
+  int32_t debug_mma;            // profiling only: 1 = no operand loads (MMAs on stale smem), 2 = also B as K-major
 };
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
@@ -240,7 +245,10 @@ constexpr int TL_TILES = 96;                          // tiles recorded per pair
 constexpr int TL_OFF = 4 * 512;                       // [pair][tile][3] = tile, start, end (ns)
 constexpr int TL_CHUNKS = 32768;                      // chunk landing times recorded
 constexpr int TL_CHUNK_OFF = TL_OFF + 128 * TL_TILES * 3;
-constexpr int PROF_WORDS = TL_CHUNK_OFF + TL_CHUNKS;
+constexpr int PS_OFF = TL_CHUNK_OFF + TL_CHUNKS;        // per CTA: producer cycles, producer waits for a free
+                                                      // stage, load latency sum (issue -> full), count, max
+constexpr int PS_WORDS = 8;
+constexpr int PROF_WORDS = PS_OFF + 160 * PS_WORDS;
 constexpr int CHUNK_FLAGS_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
 
 // Completion signal: once every tile of every op naming this slot has been
@@ -307,6 +315,11 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   uint64_t* tq_full = bars + 2 * C::STAGES + 5;     // [TQ]
   uint64_t* tq_empty = tq_full + TQ;                // [TQ] (leader CTA)
   volatile int* tq = reinterpret_cast<volatile int*>(tq_empty + TQ);  // [TQ]
+#if UM_PROFILE
+  // (profiling) clock64 at which the leader's producer issued each stage's loads
+  volatile unsigned long long* issue_ts = reinterpret_cast<volatile unsigned long long*>(tq_empty + TQ + TQ / 2);
+  static_assert((2 * C::STAGES + 5 + 2 * TQ + TQ / 2 + C::STAGES) * 8 <= C::BAR_BYTES, "barrier area");
+#endif
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -382,12 +395,18 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
-    // ===================== TMA producer (one thread per CTA) =====================
-    if (lane == 0) {
+    // ===================== TMA producer (warp 0; one elected lane issues) =====================
+    // The whole warp runs the k-block loop so the TMA operands (tensor-map
+    // address, coordinates, smem and barrier addresses) are warp-uniform: a
+    // single-thread loop paid a per-instruction uniform-register waterfall and
+    // its dependent chain (~1.5k cycles per k-block, measured) became the
+    // operand-feed limit.  Tile-queue and get/flag waits stay on lane 0.
+    {
+      const bool issuer = ptx::elect_one();
       const uint64_t pols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
       int stage = 0;
       uint32_t phase = 0;
-      uint64_t landed = 0;   // in-kernel gets whose every chunk this producer has observed
+      uint64_t landed = 0;   // (lane 0) in-kernel gets whose every chunk this producer has observed
       // fine-grained waits: rows [r0, r1) of get g's band.  Fast path: the
       // band's chunk count says it has fully landed (then never checked
       // again); otherwise the flags of the chunks holding those rows, loaded
@@ -423,36 +442,43 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         ptx::fence_proxy_async_global();
       };
-      int flag_ok = -1;      // highest work index whose external arrival flag has been observed
+      int flag_ok = -1;      // (lane 0) highest work index whose external arrival flag has been observed
       int q = 0;
+#if UM_PROFILE
+      unsigned long long p_empty = 0, p_issue = 0, p_t_issue = 0, p_tma = 0, p_loop = 0;
+      const unsigned long long p_begin = clock64();
+#endif
       for (int i = 0;; ++i) {
-        if (cleader) {
-          // take the next tile and publish it to every CTA of the cluster
-          const int slot = i % TQ;
-          ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
-          if (NP > 1 && np == 1 && (i % NP) != 0) {
-            q += 1;   // next part of the tile taken NP entries ago
+        if (lane == 0) {
+          if (cleader) {
+            // take the next tile and publish it to every CTA of the cluster
+            const int slot = i % TQ;
+            ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
+            if (NP > 1 && np == 1 && (i % NP) != 0) {
+              q += 1;   // next part of the tile taken NP entries ago
+            } else {
+              int t = (NP == 1 && works[0].sched_static) ? (int)(blockIdx.x / CS) + i * (int)(gridDim.x / CS)  // A/B knob
+                                                         : atomicAdd(tile_counter, 1);
+              if (t > total_units) t = total_units;
+              q = t * NP;
+            }
+            tq[slot] = q;
+            if constexpr (CS > 1) {
+              for (int r = 1; r < cs; ++r) ptx::st_shared_cluster_u32((const void*)&tq[slot], r, (uint32_t)q);
+              for (int r = 0; r < cs; ++r) ptx::mbar_arrive_cluster(&tq_full[slot], r);
+            } else {
+              ptx::mbar_arrive_cluster(&tq_full[slot], 0);
+            }
           } else {
-            int t = (NP == 1 && works[0].sched_static) ? (int)(blockIdx.x / CS) + i * (int)(gridDim.x / CS)  // A/B knob
-                                                       : atomicAdd(tile_counter, 1);
-            if (t > total_units) t = total_units;
-            q = t * NP;
+            q = next_tile(i);
           }
-          tq[slot] = q;
-          if constexpr (CS > 1) {
-            for (int r = 1; r < cs; ++r) ptx::st_shared_cluster_u32((const void*)&tq[slot], r, (uint32_t)q);
-            for (int r = 0; r < cs; ++r) ptx::mbar_arrive_cluster(&tq_full[slot], r);
-          } else {
-            ptx::mbar_arrive_cluster(&tq_full[slot], 0);
-          }
-        } else {
-          q = next_tile(i);
         }
+        q = __shfl_sync(0xffffffffu, q, 0);
         int t, row_off;
         decode(q, t, row_off);
-        if (i == 0) stamp(2);
+        if (i == 0 && lane == 0) stamp(2);
         if (t >= total_units) {
-          if (leader) {
+          if (leader && lane == 0) {
             // this pair is done with the counter (its cluster leader took its
             // last tile); the last pair out re-zeroes it for the next launch
             __threadfence();
@@ -461,6 +487,15 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               atomicExch(&tile_counter[1], 0);
             }
           }
+#if UM_PROFILE
+          if (args.prof && blockIdx.x < 160 && lane == 0) {
+            args.prof[PS_OFF + PS_WORDS * blockIdx.x + 0] = clock64() - p_begin;
+            args.prof[PS_OFF + PS_WORDS * blockIdx.x + 1] = p_empty;
+            args.prof[PS_OFF + PS_WORDS * blockIdx.x + 5] = p_issue;
+            args.prof[PS_OFF + PS_WORDS * blockIdx.x + 6] = p_tma;
+            args.prof[PS_OFF + PS_WORDS * blockIdx.x + 7] = p_loop;
+          }
+#endif
           break;
         }
         int w0, ukb0, ukb1;
@@ -472,56 +507,87 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         int kbg = 0;   // k-block index over the whole chain (C prefetch trigger)
         const int cpf_at = works[w0].c_prefetch > 0 && works[w0].c_remote == 0
                                ? max(0, works[w0].num_kb - works[w0].c_prefetch) : -1;
-        for (int w = w0; w < w0 + works[w0].nseg; ++w) {
+        const int nseg = works[w0].nseg;
+        // loop-invariant knobs read once per tile (the work list lives in the
+        // parameter block or global memory: no reloads inside the k loop)
+        const bool halfb = NP == 1 && C::NACC == 2 && works[0].debug_halfb;
+#if UM_PROFILE
+        const bool mma_only = works[0].debug_mma != 0;
+#endif
+        for (int w = w0; w < w0 + nseg; ++w) {
         const Work& wk = works[w];
+        const int a_col0 = wk.a_col0, b_row0 = wk.b_row0, a_fine = wk.a_fine, b_fine = wk.b_fine;
         // fused get -> GEMM: this segment reads operand slices a get is still
         // delivering; wait until every chunk of those gets has landed
-        if (wk.wait_flag && w > flag_ok) {
-          ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
-          flag_ok = w;
+        if (lane == 0) {
+          if (wk.wait_flag && w > flag_ok) {
+            ptx::wait_flag_geq(wk.wait_flag, wk.wait_value);
+            flag_ok = w;
+          }
+          for (uint64_t msk = wk.wait_mask & ~landed; msk; msk &= msk - 1) {
+            const int gi = __ffsll((long long)msk) - 1;
+            ptx::wait_count_geq(&args.counters[3 + gi], args.gets[gi].nchunks);
+          }
+          landed |= wk.wait_mask;
         }
-        for (uint64_t msk = wk.wait_mask & ~landed; msk; msk &= msk - 1) {
-          const int gi = __ffsll((long long)msk) - 1;
-          ptx::wait_count_geq(&args.counters[3 + gi], args.gets[gi].nchunks);
-        }
-        landed |= wk.wait_mask;
         const CUtensorMap* ma = &maps[3 * w + 0];
         const CUtensorMap* mbm = &maps[3 * w + 1];
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
         const int arow = wk.a_row0 + mb * BM * CG * NP + row_off;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
-        if (wk.a_fine) wait_rows(wk.a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
+        if (a_fine && lane == 0) wait_rows(a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
+        __syncwarp();
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
         // default: measured slower, 1437 -> 1143..1292 TFLOP/s on cfg2)
         auto prefetch = [&](int kb) {
-          ptx::tma_prefetch_2d(ma, wk.a_col0 + kb * BK, arow);
+          if (!issuer) return;
+          ptx::tma_prefetch_2d(ma, a_col0 + kb * BK, arow);
 #pragma unroll
           for (int j = 0; j < C::NACC; ++j)
 #pragma unroll
             for (int s = 0; s < C::SUB_PER_ACC; ++s)
-              ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, wk.b_row0 + kb * BK);
+              ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, b_row0 + kb * BK);
         };
         const int pf = wk.prefetch;
         // k-blocks of this segment; a staggered or split-k unit (single-segment
         // works only) covers [ukb0, ukb1) of its tile
         const bool piece = nstag > 0 || nsplit > 1;
         const int kbs = piece ? ukb0 : 0, kbe = piece ? ukb1 : wk.seg_kb;
-        for (int kb = kbs; kb < min(kbs + pf, kbe); ++kb) prefetch(kb);
+        if (pf > 0)
+          for (int kb = kbs; kb < min(kbs + pf, kbe); ++kb) prefetch(kb);
+#if UM_PROFILE
+        const unsigned long long p_t_loop = clock64();
+#endif
         for (int kb = kbs; kb < kbe; ++kb) {
           if (pf > 0 && kb + pf < kbe) prefetch(kb + pf);
+#if UM_PROFILE
+          {
+            const unsigned long long e0 = clock64();
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const unsigned long long e1 = clock64();
+            p_empty += e1 - e0;
+            p_t_issue = e1;
+            if (leader && lane == 0) issue_ts[stage] = e1;
+          }
+          if (mma_only) {   // (profiling) MMA-issue bound: no loads at all
+            if (leader && issuer) ptx::mbar_arrive(&full[stage]);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+#else
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          // (profiling only, UM_GEMM_DEBUG_HALFB: wrong results) skip the second
-          // accumulator's B sub-tiles -> bound on what halving B traffic can buy
-          const bool halfb = NP == 1 && C::NACC == 2 && works[0].debug_halfb;
+#endif
           constexpr uint32_t MC_MASK = NP == 4 ? 0x55u : 0x5u;   // pair rank 0 of every pair
           const bool mcast = NP > 1 && np == NP;
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (halfb ? C::B_BYTES / 2 : 0)) * CG);
-          uint8_t* sa = smem_a + stage * C::A_BYTES;
-          uint8_t* sb = smem_b + stage * C::B_BYTES;
-          const int kcol = wk.a_col0 + kb * BK;
-          const int krow = wk.b_row0 + kb * BK;
-          if (wk.b_fine) wait_rows(wk.b_fine - 1, krow, krow + BK);   // this k-block's B rows
-          if (kbg++ == cpf_at) {
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * C::A_BYTES);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+          const int kcol = a_col0 + kb * BK;
+          const int krow = b_row0 + kb * BK;
+          if (b_fine) {   // this k-block's B rows
+            if (lane == 0) wait_rows(b_fine - 1, krow, krow + BK);
+            __syncwarp();
+          }
+          if (kbg++ == cpf_at && issuer) {
             // bring this CTA's 128 x NT block of C into L2 ahead of the reduce-adds
             const Work& hd = works[w0];
             const CUtensorMap* mcp = &maps[3 * w0 + 2];
@@ -529,39 +595,60 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             for (int r = 0; r < BM; r += 32)
               for (int c = 0; c < NT; c += 32) ptx::tma_prefetch_2d(mcp, hd.c_col0 + nb * NT + c, crow + r);
           }
-          if constexpr (CG == 1) {
-            ptx::tma_load_2d(sa, ma, &full[stage], kcol, arow, pa);
-          } else {
-            ptx::tma_load_2d_cg2(sa, ma, &full[stage], kcol, arow, pa);
-          }
-#pragma unroll
-          for (int j = 0; j < C::NACC; ++j)
-#pragma unroll
-            for (int s = 0; s < C::SUB_PER_ACC; ++s) {
-              if (halfb && j == 1) continue;
-              const int qsub = j * C::SUB_PER_ACC + s;
-              uint8_t* dst = sb + qsub * SUB_BYTES;
-              const int col = bcol + j * UMMA_N + s * 64;
-              if (mcast) {
-                // the CTAs with this pair rank in the other pairs need the same B
-                // sub-tiles: each loads 1/NP of them into all (multicast)
-                if ((qsub * NP) / C::B_SUBS != pair) continue;
-                ptx::tma_load_2d_cg2_mc(dst, mbm, &full[stage], col, krow, (uint16_t)(MC_MASK << cta_rank), pb);
-              } else if constexpr (CG == 1) {
-                ptx::tma_load_2d(dst, mbm, &full[stage], col, krow, pb);
-              } else {
-                ptx::tma_load_2d_cg2(dst, mbm, &full[stage], col, krow, pb);
-              }
+#if UM_PROFILE
+          const unsigned long long p_t_tma = clock64();
+#endif
+          if (issuer) {
+            // (profiling only, UM_GEMM_DEBUG_HALFB: wrong results) skip the second
+            // accumulator's B sub-tiles -> bound on what halving B traffic can buy
+            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], (C::STAGE_BYTES - (halfb ? C::B_BYTES / 2 : 0)) * CG);
+            if constexpr (CG == 1) {
+              ptx::tma_load_2d_s(sa, ma, &full[stage], kcol, arow, pa);
+            } else {
+              ptx::tma_load_2d_cg2_s(sa, ma, &full[stage], kcol, arow, pa);
             }
-          if (i == 0 && kb == 0) stamp(3);
+#pragma unroll
+            for (int j = 0; j < C::NACC; ++j)
+#pragma unroll
+              for (int s = 0; s < C::SUB_PER_ACC; ++s) {
+                if (halfb && j == 1) continue;
+                const int qsub = j * C::SUB_PER_ACC + s;
+                const uint32_t dst = sb + qsub * SUB_BYTES;
+                const int col = bcol + j * UMMA_N + s * 64;
+                if (mcast) {
+                  // the CTAs with this pair rank in the other pairs need the same B
+                  // sub-tiles: each loads 1/NP of them into all (multicast)
+                  if ((qsub * NP) / C::B_SUBS != pair) continue;
+                  ptx::tma_load_2d_cg2_mc_s(dst, mbm, &full[stage], col, krow, (uint16_t)(MC_MASK << cta_rank), pb);
+                } else if constexpr (CG == 1) {
+                  ptx::tma_load_2d_s(dst, mbm, &full[stage], col, krow, pb);
+                } else {
+                  ptx::tma_load_2d_cg2_s(dst, mbm, &full[stage], col, krow, pb);
+                }
+              }
+          }
+          if (i == 0 && kb == 0 && lane == 0) stamp(3);
+#if UM_PROFILE
+          {
+            const unsigned long long p_now = clock64();
+            p_issue += p_now - p_t_issue;
+            p_tma += p_now - p_t_tma;
+          }
+#endif
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+#if UM_PROFILE
+        p_loop += clock64() - p_t_loop;
+#endif
         }  // k-chain segments
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread, leader CTA) =====================
-    if (leader && lane == 0) {
+    // ===================== MMA issuer (leader CTA; one elected lane issues) =====================
+    // The whole warp runs the loop (barrier waits, descriptor arithmetic) so
+    // every operand of tcgen05.mma is warp-uniform; one elected lane issues.
+    if (leader) {
+      const bool issuer = ptx::elect_one();
       constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 1);
       // a stage is free once every pair sharing its B (multicast) has consumed it
       const uint16_t EMPTY_MASK = (uint16_t)((1u << cs) - 1);
@@ -571,6 +658,26 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       int it = 0;
       unsigned long long c_full = 0, c_tmem = 0, c_tile = 0;
       const unsigned long long c_begin = clock64();
+#if UM_PROFILE
+      unsigned long long l_sum = 0, l_cnt = 0, l_max = 0;
+#endif
+      // (profiling) wait for a stage's operands and account the issue -> landed latency
+      auto wait_full = [&](int stg, uint32_t ph) {
+#if UM_PROFILE
+        if (args.prof) {
+          const unsigned long long t0 = clock64();
+          ptx::mbar_wait(&full[stg], ph);
+          const unsigned long long t1 = clock64();
+          c_full += t1 - t0;
+          const unsigned long long lat = t1 - issue_ts[stg];
+          l_sum += lat;
+          ++l_cnt;
+          l_max = lat > l_max ? lat : l_max;
+          return;
+        }
+#endif
+        ptx::mbar_wait(&full[stg], ph);
+      };
       auto timed = [&](unsigned long long& acc, auto&& fn) {
 #if UM_PROFILE
         if (args.prof) {
@@ -589,6 +696,18 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       auto issue = [&](int stg, uint32_t acc_col, int j, bool first_kb) {
         const uint32_t sa = ptx::smem_u32(smem_a + stg * C::A_BYTES);
         const uint32_t sb = ptx::smem_u32(smem_b + stg * C::B_BYTES) + j * C::SUB_PER_ACC * SUB_BYTES;
+#if UM_PROFILE
+        if (works[0].debug_mma == 2) {   // (profiling) B read as K-major SW128: UMMA rate vs operand major-ness
+          constexpr uint32_t idesc_k = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 0);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
+            const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 2), 16, 1024);
+            if (issuer) ptx::umma_f16<CG>(tmem_base + acc_col, adesc, bdesc, idesc_k, (!first_kb || kk) ? 1u : 0u);
+          }
+          return;
+        }
+#endif
 #pragma unroll
         for (int kk = 0; kk < BK / UMMA_K; ++kk) {
           // A: K-major SW128, 8-row groups 1024 B apart; advance 32 B per UMMA_K.
@@ -596,17 +715,18 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           // B: MN-major SW128; 64-column blocks SUB_BYTES apart (LBO), 8-k groups
           // 1024 B apart (SBO); advance 16 k-rows = 2048 B per UMMA_K.
           const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 128), SUB_BYTES, 1024);
-          ptx::umma_f16<CG>(tmem_base + acc_col, adesc, bdesc, idesc, (!first_kb || kk) ? 1u : 0u);
+          if (issuer) ptx::umma_f16<CG>(tmem_base + acc_col, adesc, bdesc, idesc, (!first_kb || kk) ? 1u : 0u);
         }
       };
       for (;; ++it) {
         int t = 0, row_off_unused;
-        timed(c_tile, [&] { t = next_tile(it); });
+        if (lane == 0) timed(c_tile, [&] { t = next_tile(it); });
+        t = __shfl_sync(0xffffffffu, t, 0);
         decode(t, t, row_off_unused);
         if (t >= total_units) break;
 #if UM_PROFILE
         const int tl_pair = (int)(blockIdx.x / CG);
-        if (args.prof && it < TL_TILES && tl_pair < 128) {
+        if (args.prof && it < TL_TILES && tl_pair < 128 && lane == 0) {
           unsigned long long* e = args.prof + TL_OFF + (tl_pair * TL_TILES + it) * 3;
           e[0] = (unsigned long long)t + 1;
           e[1] = ptx::globaltimer();
@@ -621,11 +741,11 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           timed(c_tmem, [&] { ptx::mbar_wait(&tmem_empty[buf], tph ^ 1); });
           ptx::tc_fence_after();
           for (int kb = 0; kb < num_kb; ++kb) {
-            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
-            if (it == 0 && kb == 0) stamp(4);
+            wait_full(stage, phase);
+            if (it == 0 && kb == 0 && lane == 0) stamp(4);
             ptx::tc_fence_after();
             issue(stage, buf * UMMA_N, 0, kb == 0);
-            ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
+            if (issuer) ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
         } else {
@@ -637,7 +757,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           ptx::tc_fence_after();
           const int stage0 = stage;
           for (int kb = 0; kb < D; ++kb) {
-            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
+            wait_full(stage, phase);
             ptx::tc_fence_after();
             issue(stage, 0, 0, kb == 0);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -647,49 +767,56 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           int st = stage0;
           for (int kb = 0; kb < D; ++kb) {
             issue(st, UMMA_N, 1, kb == 0);
-            ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
+            if (issuer) ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
           // accumulator 0 also finishes E k-blocks early, so its drain overlaps
           // accumulator 1's tail
           const int E = works[0].no_end_stagger ? 0 : min(SG, num_kb - D);
           for (int kb = D; kb < num_kb - E; ++kb) {
-            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
+            wait_full(stage, phase);
             ptx::tc_fence_after();
             issue(stage, 0, 0, kb == 0);          // kb == 0 only without a leading stagger (D == 0)
             issue(stage, UMMA_N, 1, kb == 0);
-            ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
+            if (issuer) ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
           const int stageE = stage;
           for (int kb = num_kb - E; kb < num_kb; ++kb) {
-            timed(c_full, [&] { ptx::mbar_wait(&full[stage], phase); });
+            wait_full(stage, phase);
             ptx::tc_fence_after();
             issue(stage, 0, 0, false);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::umma_commit<CG>(&tmem_full[0], PAIR_MASK);
+          if (issuer) ptx::umma_commit<CG>(&tmem_full[0], PAIR_MASK);
           st = stageE;
           for (int kb = num_kb - E; kb < num_kb; ++kb) {
             issue(st, UMMA_N, 1, false);
-            ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
+            if (issuer) ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
-          ptx::umma_commit<CG>(&tmem_full[1], PAIR_MASK);
+          if (issuer) ptx::umma_commit<CG>(&tmem_full[1], PAIR_MASK);
         }
-        if constexpr (C::NACC == 1) ptx::umma_commit<CG>(&tmem_full[buf], PAIR_MASK);
-        if (it == 0) stamp(5);
+        if constexpr (C::NACC == 1) if (issuer) ptx::umma_commit<CG>(&tmem_full[buf], PAIR_MASK);
+        if (it == 0 && lane == 0) stamp(5);
 #if UM_PROFILE
-        if (args.prof && it < TL_TILES && tl_pair < 128)   // all MMAs of the tile issued
+        if (args.prof && it < TL_TILES && tl_pair < 128 && lane == 0)   // all MMAs of the tile issued
           args.prof[TL_OFF + (tl_pair * TL_TILES + it) * 3 + 2] = ptx::globaltimer();
 #endif
       }
-      if (args.prof) {
+      if (args.prof && lane == 0) {
         unsigned long long* o = args.prof + 4 * (blockIdx.x / CG);
         o[0] = clock64() - c_begin;
         o[1] = c_full;
         o[2] = c_tmem;
         o[3] = c_tile | ((unsigned long long)cs << 56);   // + this cluster's size
+#if UM_PROFILE
+        if (blockIdx.x < 160) {
+          args.prof[PS_OFF + PS_WORDS * blockIdx.x + 2] = l_sum;
+          args.prof[PS_OFF + PS_WORDS * blockIdx.x + 3] = l_cnt;
+          args.prof[PS_OFF + PS_WORDS * blockIdx.x + 4] = l_max;
+        }
+#endif
       }
     }
   } else if (warp < 2 + EW) {
@@ -1418,8 +1545,10 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     w.stagger = kn.stagger;
 #if UM_PROFILE
     w.debug_halfb = env_int("UM_GEMM_DEBUG_HALFB", 0) ? 1 : 0;   // profiling build only: wrong results
+    w.debug_mma = env_int("UM_GEMM_DEBUG_MMA", 0);                // profiling build only: wrong results
 #else
     w.debug_halfb = 0;
+    w.debug_mma = 0;
 #endif
     w.a_fine = op.a_get;
     w.b_fine = op.b_get;
@@ -1770,6 +1899,20 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
               (h[TRACE_OFF + 5] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 6] - h[TRACE_OFF]) * 1e-3,
               (h[TRACE_OFF + 7] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 8] - h[TRACE_OFF]) * 1e-3,
               (h[TRACE_OFF + 9] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 10] - h[TRACE_OFF]) * 1e-3);
+    }
+    {
+      double pt = 0, pe = 0, pi = 0, ptm = 0, pl = 0, ls = 0, lc = 0, lm = 0;
+      int np_ = 0;
+      for (int b = 0; b < 160; ++b) {
+        const unsigned long long* e = &h[PS_OFF + PS_WORDS * b];
+        if (e[0]) { pt += e[0]; pe += e[1]; pi += e[5]; ptm += e[6]; pl += e[7]; ++np_; }
+        if (e[3]) { ls += e[2]; lc += e[3]; lm = std::max(lm, (double)e[4]); }
+      }
+      if (np_ && lc)
+        fprintf(stderr, "[um_gemm stalls] producers wait for a free stage %.1f %% and issue loads %.1f %% of their "
+                        "cycles (of which the TMA instructions %.1f %%; the k-block loops %.1f %%); operand load latency "
+                        "(leader issue -> stage full) mean %.0f, max %.0f cycles over %.0f stages\n",
+                100 * pe / pt, 100 * pi / pt, 100 * ptm / pt, 100 * pl / pt, ls / lc, lm, lc);
     }
     if (n)
       fprintf(stderr, "[um_gemm stalls] %d pairs (%d in clusters > 2), MMA thread: waiting for operands %.1f %%, for TMEM (epilogue) "

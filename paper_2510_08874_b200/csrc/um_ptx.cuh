@@ -172,6 +172,17 @@ __device__ __forceinline__ void st_shared_cluster_u32(const void* local, uint32_
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// One lane of a converged warp (the lowest active one, i.e. always the same
+// lane): tcgen05.mma / tcgen05.commit issue under it while the whole warp runs
+// the control flow, so descriptors stay warp-uniform (uniform registers, no
+// per-instruction waterfall loop around UTCHMMA).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -224,6 +235,34 @@ __device__ __forceinline__ void tma_load_2d_cg2_mc(void* smem_dst, const void* t
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
       ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+// The same loads with the destination given as a shared-memory address (u32):
+// a warp-uniform value the compiler keeps in a uniform register.
+__device__ __forceinline__ void tma_load_2d_s(uint32_t smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2_s(uint32_t smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
+                                                  int32_t c1, uint64_t policy) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
+      "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2_mc_s(uint32_t smem_dst, const void* tmap, uint64_t* bar, int32_t c0,
+                                                     int32_t c1, uint16_t mask, uint64_t policy) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_dst),
       "l"(tmap), "r"(bar_leader), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
       : "memory");
 }
