@@ -238,6 +238,11 @@ constexpr int MAX_CHUNK_FLAGS = 1 << 16;  // per-chunk landed flags (fine-graine
 #ifndef UM_PROFILE
 #define UM_PROFILE 0
 #endif
+// UM_VARIANTS=1 (`make variant`): the rejected kernel variants (cta_group::1,
+// B multicast, 8 epilogue warps) without the profiling code, for A/B timing
+#ifndef UM_VARIANTS
+#define UM_VARIANTS 0
+#endif
 constexpr int TRACE_OFF = 4 * 512 - 16;   // profiling timeline stamps inside the prof buffer
 // UM_GEMM_TIMELINE=<csv> (profiling build): per-pair tile spans and per-chunk
 // landing times of the in-kernel pulls, after the stall counters
@@ -830,6 +835,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     uint64_t cpol = cpols[0];
     uint8_t* ebuf = smem_epi + e * C::EPI_BOXES * EPI_BOX_BYTES;
     const uint32_t ebuf_u32 = ptx::smem_u32(ebuf);
+    const bool issuer = ptx::elect_one();   // issues this warp's bulk (TMA) ops; uniform operands
     int it = 0;
     int sbuf = 0;
     for (;; ++it) {
@@ -841,7 +847,8 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       t = unit_span(works, nwork, total_tiles, nstag, nsplit, t, w, ukb0_unused, ukb1_unused);
       const Work& wk = works[w];
       const CUtensorMap* mc = &maps[3 * w + 2];
-      if (wk.c_pol >= 0) cpol = cpols[wk.c_pol];
+      const int c_remote = wk.c_remote, c_col0 = wk.c_col0, c_row0 = wk.c_row0, c_pol = wk.c_pol;
+      if (c_pol >= 0) cpol = cpols[c_pol];
       int mb, nb;
       tile_coords(wk, t - wk.tile_start, mb, nb);
       const int buf = it % C::NBUF;
@@ -850,11 +857,11 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
 
       // one 32x32 fp32 chunk (lane = row) from registers into C
       auto emit = [&](const uint32_t (&r)[32], int col0) {
-        if (wk.c_remote == 3) return;  // (profiling only) accumulator dropped: isolates the main loop's cost
-        if (lane == 0) ptx::bulk_wait_read<C::EPI_BOXES - 1>();   // box no longer read by an earlier TMA op
+        if (c_remote == 3) return;  // (profiling only) accumulator dropped: isolates the main loop's cost
+        if (issuer) ptx::bulk_wait_read<C::EPI_BOXES - 1>();   // box no longer read by an earlier TMA op
         __syncwarp();
         const uint32_t base = ebuf_u32 + sbuf * EPI_BOX_BYTES;
-        if (wk.c_remote != 1) {
+        if (c_remote != 1) {
           // registers -> swizzled smem box -> TMA reduce-add into C
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -862,14 +869,14 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
                               r[4 * i + 3]);
           ptx::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (issuer) {
             uint8_t* box = ebuf + sbuf * EPI_BOX_BYTES;
-            if (wk.c_remote == 2)  // (profiling only) plain store instead of reduce
-              ptx::tma_store_2d(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op);
-            else if (wk.c_pol >= 0)
-              ptx::tma_reduce_add_2d_hint(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op, cpol);
+            if (c_remote == 2)  // (profiling only) plain store instead of reduce
+              ptx::tma_store_2d(mc, box, c_col0 + col0, c_row0 + row_in_op);
+            else if (c_pol >= 0)
+              ptx::tma_reduce_add_2d_hint(mc, box, c_col0 + col0, c_row0 + row_in_op, cpol);
             else
-              ptx::tma_reduce_add_2d(mc, box, wk.c_col0 + col0, wk.c_row0 + row_in_op);
+              ptx::tma_reduce_add_2d(mc, box, c_col0 + col0, c_row0 + row_in_op);
             ptx::bulk_commit();
           }
         } else {
@@ -884,7 +891,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           __syncwarp();
           const int c4 = lane & 7;          // 16-byte column group of this lane
           const int col = col0 + 4 * c4;
-          if (wk.c_remote == 4 && wk.c_vec_ok && col0 + 32 <= wk.n && row_in_op + 32 <= wk.m) {
+          if (c_remote == 4 && wk.c_vec_ok && col0 + 32 <= wk.n && row_in_op + 32 <= wk.m) {
             // exclusive writer: plain read-modify-write through the load/store
             // units (the TMA unit stays free for the producer's operand loads);
             // 8 independent 16-byte loads in flight per lane
@@ -1153,7 +1160,7 @@ static const Knobs& knobs() {
   static Knobs k;
   static std::once_flag once;
   std::call_once(once, [] {
-#if UM_PROFILE
+#if UM_PROFILE || UM_VARIANTS
     // variants measured and rejected (cta_group::1, B multicast across pairs,
     // 8 epilogue warps) are instantiated in the profiling build only
     k.cg = env_int("UM_GEMM_CG", 2) == 1 ? 1 : 2;
@@ -1168,7 +1175,7 @@ static const Knobs& knobs() {
     k.cpol = env_int("UM_GEMM_CPOL", -1);
     k.prefetch = std::max(0, env_int("UM_GEMM_PF", 0));
     k.sched_static = env_int("UM_GEMM_STATIC", 0) ? 1 : 0;
-#if UM_PROFILE
+#if UM_PROFILE || UM_VARIANTS
     k.epi_warps = env_int("UM_GEMM_EPI_WARPS", 4) == 8 ? 8 : 4;
     k.pairs = env_int("UM_GEMM_PAIRS", 1);
     if (k.pairs != 2 && k.pairs != 4) k.pairs = 1;
@@ -1835,7 +1842,7 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   args.prof = prof;
   int rc;
   const bool g = P->ngets > 0;
-#if UM_PROFILE
+#if UM_PROFILE || UM_VARIANTS
   if (P->CG == 1) rc = g ? launch<1, 256, 4, GET_WARPS>(args, P->device, stream) : launch<1, 256, 4, 0>(args, P->device, stream);
   else if (P->NT == 512 && P->NP == 2)
     rc = g ? launch<2, 512, 4, GET_WARPS, 2>(args, P->device, stream) : launch<2, 512, 4, 0, 2>(args, P->device, stream);
