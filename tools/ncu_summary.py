@@ -1,4 +1,8 @@
-"""Summarise ncu --set full reports (gpurun_out/*.ncu-rep) into profiles/r1_ncu_summary.json."""
+"""Summarise ncu --set full reports (gpurun_out/*.ncu-rep) into a profiles/ summary
+(default profiles/r1_ncu_summary.json; UM_NCU_SUMMARY=<name> picks another file),
+each entry stamped with the kernel build's git SHA and the date.
+
+    python tools/ncu_summary.py label=gpurun_out/x.ncu-rep="command" ..."""
 import csv
 import json
 import os
@@ -38,11 +42,15 @@ def summarise(rep, command):
 
 if __name__ == '__main__':
     # args: label=report=command ...
-    out_path = os.path.join(ROOT, 'profiles', 'r1_ncu_summary.json')
+    out_path = os.path.join(ROOT, 'profiles', os.environ.get('UM_NCU_SUMMARY', 'r1_ncu_summary.json'))
     out = {}
+    sha = subprocess.run(['git', '-C', ROOT, 'rev-parse', '--short', 'HEAD'], capture_output=True, text=True).stdout.strip()
+    import datetime
     for arg in sys.argv[1:]:
         label, rep, cmd = arg.split('=', 2)
         out[label] = summarise(rep, cmd)
+        out[label].update({'git_sha': sha, 'date': datetime.date.today().isoformat(),
+                           'capture': 'ncu --set full --clock-control none (one B200)'})
     json.dump(out, open(out_path, 'w'), indent=1)
     for k, v in out.items():
         print(k, v.get('gpu__time_duration.sum'), f"{v['dram_bytes_per_launch'] / 1e9:.2f} GB",
