@@ -109,7 +109,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-struct alignas(16) Work {
+struct alignas(16) Work {   // sizeof is a multiple of 16 (setup touches it as uint4)
   int32_t m, n, k;
   int32_t tiles_m, tiles_n, num_kb;
   int32_t tile_start, c_remote;
@@ -393,6 +393,18 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   // warm the descriptors of the first works while the CTA sets up (the first
   // TMA otherwise waits for its tensor map: ~1 us of a small launch)
   if (warp == 0 && lane < 3 * 8 && lane / 3 < nwork) ptx::prefetch_tmap(&maps[lane]);
+  // ... and the first works themselves: every role's first tile reads them
+  // through a chain of dependent scalar loads, each a cold miss (~1 us) when
+  // the work list sits in the parameter block; one parallel touch here (32
+  // lanes x 16 B) brings them into the SM's caches during setup
+  if (warp == 2 || warp == 3) {
+    const int nvec = min(nwork, 8) * (int)(sizeof(Work) / 16);
+    const int v = (warp - 2) * 32 + lane;
+    if (v < nvec) {
+      const volatile uint4* wv = reinterpret_cast<const volatile uint4*>(works) + v;
+      (void)wv->x;
+    }
+  }
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             // take the next tile and publish it to every CTA of the cluster
             const int slot = i % TQ;
             ptx::mbar_wait_cluster(&tq_empty[slot], ((uint32_t)(i / TQ) & 1u) ^ 1u);
+            if (i == 0) stamp(11);
             if (NP > 1 && np == 1 && (i % NP) != 0) {
               q += 1;   // next part of the tile taken NP entries ago
             } else {
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               if (t > total_units) t = total_units;
               q = t * NP;
             }
+            if (i == 0) stamp(12);
             tq[slot] = q;
             if constexpr (CS > 1) {
               for (int r = 1; r < cs; ++r) ptx::st_shared_cluster_u32((const void*)&tq[slot], r, (uint32_t)q);
@@ -508,14 +522,17 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
         int w0, ukb0, ukb1;
         t = unit_span(works, nwork, total_tiles, nstag, nsplit, t, w0, ukb0, ukb1);
+        // the head work by value: independent vector loads instead of a chain
+        // of dependent scalar ones through the parameter block
+        const Work W0 = works[w0];
         int mb, nb;
-        tile_coords(works[w0], t - works[w0].tile_start, mb, nb);
+        tile_coords(W0, t - W0.tile_start, mb, nb);
+        if (i == 0 && lane == 0) stamp(13);
         // a k-chain: the segments (ops with the same C region) are loaded one
         // after the other into the same accumulator, one epilogue per tile
         int kbg = 0;   // k-block index over the whole chain (C prefetch trigger)
-        const int cpf_at = works[w0].c_prefetch > 0 && works[w0].c_remote == 0
-                               ? max(0, works[w0].num_kb - works[w0].c_prefetch) : -1;
-        const int nseg = works[w0].nseg;
+        const int cpf_at = W0.c_prefetch > 0 && W0.c_remote == 0 ? max(0, W0.num_kb - W0.c_prefetch) : -1;
+        const int nseg = W0.nseg;
         // loop-invariant knobs read once per tile (the work list lives in the
         // parameter block or global memory: no reloads inside the k loop)
         const bool halfb = NP == 1 && C::NACC == 2 && works[0].debug_halfb;
@@ -523,7 +540,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const bool mma_only = works[0].debug_mma != 0;
 #endif
         for (int w = w0; w < w0 + nseg; ++w) {
-        const Work& wk = works[w];
+        const Work wk = w == w0 ? W0 : works[w];
         const int a_col0 = wk.a_col0, b_row0 = wk.b_row0, a_fine = wk.a_fine, b_fine = wk.b_fine;
         // fused get -> GEMM: this segment reads operand slices a get is still
         // delivering; wait until every chunk of those gets has landed
@@ -563,6 +580,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const int kbs = piece ? ukb0 : 0, kbe = piece ? ukb1 : wk.seg_kb;
         if (pf > 0)
           for (int kb = kbs; kb < min(kbs + pf, kbe); ++kb) prefetch(kb);
+        if (i == 0 && lane == 0) stamp(14);
 #if UM_PROFILE
         const unsigned long long p_t_loop = clock64();
 #endif
@@ -1909,6 +1927,10 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
               (h[TRACE_OFF + 5] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 6] - h[TRACE_OFF]) * 1e-3,
               (h[TRACE_OFF + 7] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 8] - h[TRACE_OFF]) * 1e-3,
               (h[TRACE_OFF + 9] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 10] - h[TRACE_OFF]) * 1e-3);
+      fprintf(stderr, "[um_gemm stalls] block 0 producer (us): tile-queue slot free %.2f, unit taken %.2f, coordinates "
+                      "%.2f, segment set up %.2f\n", (h[TRACE_OFF + 11] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 12] - h[TRACE_OFF]) * 1e-3, (h[TRACE_OFF + 13] - h[TRACE_OFF]) * 1e-3,
+              (h[TRACE_OFF + 14] - h[TRACE_OFF]) * 1e-3);
     }
     {
       double pt = 0, pe = 0, pi = 0, ptm = 0, pl = 0, ls = 0, lc = 0, lm = 0;
