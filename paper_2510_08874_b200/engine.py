@@ -8,6 +8,7 @@ pool, the copy-engine pulls, and one prepared K1 launch per group
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -38,6 +39,12 @@ def _join_current(fabric, events):
         cur = torch.cuda.current_stream(d)
         for ev in events:
             cur.wait_event(ev)
+
+
+# profiling knob (UM_DEBUG_NO_PULLS=1): launches drop their in-kernel pulls and
+# waits, so a rank's op list runs as if every operand were already staged --
+# the compute-only bound of the same launch (results are wrong)
+_NO_PULLS = os.environ.get("UM_DEBUG_NO_PULLS") == "1"
 
 
 class _IssuePlan:
@@ -221,7 +228,13 @@ class _RankRun:
                 garr[gi].src, garr[gi].dst = fetch_views(j, bands[j][k])
                 launched.add((j, k))
             h = ctypes.c_void_p()
-            _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, len(batch_gets), self.dev, ctypes.byref(h)),
+            ng = len(batch_gets)
+            if _NO_PULLS:                # profiling only: operands treated as resident (stale staging, wrong C)
+                for g in arr:
+                    g.a_get = g.b_get = 0
+                    g.get_mask = 0
+                ng = 0
+            _capi.check(lib.um_gemm_prepare(arr, len(batch), garr, ng, self.dev, ctypes.byref(h)),
                         "um_gemm_prepare")
             plan.handles.append(h.value)
             flops = float(sum(2 * (g.a.row_hi - g.a.row_lo) * (g.a.col_hi - g.a.col_lo) * (g.b.col_hi - g.b.col_lo)
