@@ -1039,7 +1039,30 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       const int r0 = (c - g.chunk_start) * g.rows_per_chunk;
       const int r1 = min(g.rows, r0 + g.rows_per_chunk);
       constexpr int U = 16;  // 16-byte loads in flight per lane (4 warps: 32 KiB per SM)
-      if (g.vec) {
+      if (g.vec == 2) {
+        // 32-byte rows: 256-bit loads / stores (half the instructions per byte
+        // of the 16-byte path, twice the bytes in flight: 8 x 32 B per lane);
+        // (row, column) advanced incrementally, no division per element
+        constexpr int U2 = 8;
+        const int n32 = g.row_bytes >> 5;
+        const int total = (r1 - r0) * n32;
+        int rr = lane / n32, cc = lane - rr * n32;
+        for (int base = lane; base < total; base += 32 * U2) {
+          uint32_t v[U2][8];
+          int pr[U2], pc[U2];
+#pragma unroll
+          for (int u = 0; u < U2; ++u) {
+            pr[u] = rr;
+            pc[u] = cc;
+            if (base + u * 32 < total) ptx::ld_nc_v8(g.src + (int64_t)(r0 + rr) * g.src_pitch + cc * 32, v[u]);
+            cc += 32;
+            while (cc >= n32) { cc -= n32; ++rr; }
+          }
+#pragma unroll
+          for (int u = 0; u < U2; ++u)
+            if (base + u * 32 < total) ptx::st_v8(g.dst + (int64_t)(r0 + pr[u]) * g.dst_pitch + pc[u] * 32, v[u]);
+        }
+      } else if (g.vec) {
         // flat (row, 16-byte column) walk of the chunk; the division by the row
         // width is a float reciprocal + one-step fix-up (exact: i < 2^24)
         const int n16 = g.row_bytes >> 4;
@@ -1784,8 +1807,12 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     g.nchunks = g.rows && g.row_bytes ? (g.rows + g.rows_per_chunk - 1) / g.rows_per_chunk : 0;
     g.chunk_start = chunks;
     g.row0 = (int32_t)gd.dst.row_lo;
-    g.vec = ((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) | (uintptr_t)g.src_pitch |
-              (uintptr_t)g.dst_pitch | (uintptr_t)g.row_bytes) & 15) == 0;
+    {
+      const uintptr_t al = reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) |
+                           (uintptr_t)g.src_pitch | (uintptr_t)g.dst_pitch | (uintptr_t)g.row_bytes;
+      // 2: 32-byte rows (256-bit loads / stores), 1: 16-byte rows, 0: 2-byte granules
+      g.vec = (al & 31) == 0 ? 2 : (al & 15) == 0 ? 1 : 0;
+    }
     chunks += g.nchunks;
   }
   args.ngets = ngets;
