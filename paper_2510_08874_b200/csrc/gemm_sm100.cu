@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       if (wk.slot >= 0) {
         // this warp's share of the tile is in C: complete its bulk writes, then
         // count it; the last arrival of the slot publishes the signal
-        if (lane == 0) ptx::bulk_wait<0>();
+        if (issuer) ptx::bulk_wait<0>();   // the bulk groups are the issuing lane's
         ptx::fence_proxy_async_global();
         __threadfence_system();
         __syncwarp();
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         }
       }
     }
-    if (lane == 0) ptx::bulk_wait<0>();
+    if (issuer) ptx::bulk_wait<0>();
     if (e == 0 && lane == 0) stamp(8);
   } else if (args.ngets > 0) {
     // ===================== get engine (GET_WARPS warps per CTA) =====================
