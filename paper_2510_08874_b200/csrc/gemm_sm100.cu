@@ -386,10 +386,20 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     else ptx::mbar_arrive_cluster(&tq_empty[slot], 0);
     return t;
   };
+  if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the setup above touches only this CTA's
+  // shared memory and TMEM, so it may overlap the previous kernel's tail on
+  // the stream (launched with programmatic stream serialization); every
+  // global access comes after the wait for that kernel's completion.
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int s = 0; s < args.nslots; ++s)   // a slot whose ops have no tile is complete at once
       if (args.slots[s].expected == 0) ptx::red_release_sys_add_u32(args.slots[s].flag, args.slots[s].increment);
-  if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
   // warm the descriptors of the first works while the CTA sets up (the first
   // TMA otherwise waits for its tensor map: ~1 us of a small launch)
   if (warp == 0 && lane < 3 * 8 && lane / 3 < nwork) ptx::prefetch_tmap(&maps[lane]);
@@ -405,10 +415,6 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       (void)wv->x;
     }
   }
-  ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
@@ -1194,6 +1200,7 @@ struct Knobs {
   int pairs = 1;
   int chain = 1;
   int chain_waves = 6;
+  int pdl = 1;
   int tail_split = 0;
   int cpf = 0;
   int stagger = 0;
@@ -1229,6 +1236,7 @@ static const Knobs& knobs() {
 #endif
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
+    k.pdl = env_int("UM_GEMM_PDL", 1) ? 1 : 0;
     k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
@@ -1347,17 +1355,30 @@ static int launch(LaunchArgs& args, int device, cudaStream_t stream) {
   cfg.blockDim = dim3(C::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (NP > 1 && fixed) ? CG * NP : CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributePreferredClusterDimension;
-  attr[1].val.preferredClusterDim.x = CG * NP;
-  attr[1].val.preferredClusterDim.y = 1;
-  attr[1].val.preferredClusterDim.z = 1;
+  cudaLaunchAttribute attr[3];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = (NP > 1 && fixed) ? CG * NP : CG;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (NP > 1 && !fixed) {
+    attr[na].id = cudaLaunchAttributePreferredClusterDimension;
+    attr[na].val.preferredClusterDim.x = CG * NP;
+    attr[na].val.preferredClusterDim.y = 1;
+    attr[na].val.preferredClusterDim.z = 1;
+    ++na;
+  }
+  // programmatic dependent launch (the kernel waits with griddepcontrol.wait
+  // before its first global access): back-to-back launches overlap one's
+  // setup with the previous one's drain.  UM_GEMM_PDL=0 turns it off.
+  if (knobs().pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (NP > 1 && !fixed) ? 2 : 1;
+  cfg.numAttrs = na;
   UM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<CG, NT, EW, GW, NP>, args));
   return UM_OK;
 }
