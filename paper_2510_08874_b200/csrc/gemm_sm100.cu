@@ -147,10 +147,16 @@ struct alignas(16) GetDesc {
   int32_t row0, pad_;             // first row of the band in its staging buffer (fine-grained waits)
 };
 
+// the work whose tile range holds tile t: the last work with tile_start <= t
+// (binary search: a launch can carry > 100 works, e.g. row-sliced ops)
 __device__ __forceinline__ int find_work(const Work* works, int nwork, int t) {
-  int w = 0;
-  while (w + 1 < nwork && works[w + 1].tile_start <= t) ++w;
-  return w;
+  int lo = 0, hi = nwork - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (works[mid].tile_start <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 // Rasterisation: tiles are walked in groups of `group` consecutive m-tiles

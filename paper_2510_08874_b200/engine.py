@@ -106,7 +106,7 @@ class _RankRun:
         """This rank's issue plan, built once per schedule and knob set (cached on the schedule)."""
         key = (self.cfg.get_engine, self.cfg.gemm_batch, self.cfg.max_inflight_accums, self.cfg.fused_accumulate,
                self.cfg.fine_waits,
-               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, self.signals_key,
+               self.cfg.k_split, self.cfg.mn_split, self.cfg.chain_order, _sch._SPLIT_BYTES, _sch._SPLIT_MIN, _sch._RASTER_N, self.signals_key,
                self.cfg.pool_capacity, self.cfg.prefetch_depth if self.cfg.pool_capacity else 0,
                self.cfg.max_inflight_gemms if self.cfg.pool_capacity else 0)
         plans = self.sched.__dict__.setdefault("plans", {})

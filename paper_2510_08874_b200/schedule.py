@@ -131,6 +131,9 @@ def lower_direct(A, B, C, cfg: ExecConfig, caller: int, ops: list | None = None)
 
 
 _SPLIT_BYTES = 64 << 20       # an op whose first use pulls at least this much runs as sub-ops
+# row-sliced ops (overlapped replica reduction) are also cut into column
+# pieces this wide and walked piece-major (0 = off; UM_RASTER_N overrides)
+_RASTER_N = int(__import__("os").environ.get("UM_RASTER_N", "2048"))
 _SPLIT_MIN = 2048             # minimum extent of a sub-op along the split dimension
 
 
@@ -193,9 +196,19 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: di
                     and nlen >= 2 * _SPLIT_MIN):
                 sn = min(cfg.mn_split, nlen // _SPLIT_MIN)
                 nc = [nlen * t // sn // 64 * 64 for t in range(sn)] + [nlen]
-            for t in range(len(cuts_i) - 1):
-                for b_ in range(len(nc) - 1):
-                    items.append((i, t * (len(nc) - 1) + b_, cuts_i[t], cuts_i[t + 1], nc[b_], nc[b_ + 1], 0, klen))
+            raster = False
+            if len(nc) == 2 and _RASTER_N and nlen >= 2 * _RASTER_N and len(cuts_i) > 2:
+                # B read in place: cut n into _RASTER_N-wide pieces and walk the
+                # row slices piece by piece, so the launch runs like one op in
+                # K1's raster (a few n-tiles of B hot in L2 over the m sweep)
+                # instead of every row slice streaming all of B
+                nc = list(range(0, nlen, _RASTER_N)) + [nlen]
+                raster = True
+            R, Cn = len(cuts_i) - 1, len(nc) - 1
+            cells = ([(t, b_) for b_ in range(Cn) for t in range(R)] if raster
+                     else [(t, b_) for t in range(R) for b_ in range(Cn)])
+            for t, b_ in cells:
+                items.append((i, t * Cn + b_, cuts_i[t], cuts_i[t + 1], nc[b_], nc[b_ + 1], 0, klen))
             continue
         if not unfused_remote and pa + pb >= _SPLIT_BYTES:
             if (cfg.k_split <= 1 and cfg.mn_split > 1 and min(pa, pb) >= _SPLIT_BYTES // 2
