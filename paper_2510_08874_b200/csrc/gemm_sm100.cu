@@ -1837,8 +1837,15 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     {
       const uintptr_t al = reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) |
                            (uintptr_t)g.src_pitch | (uintptr_t)g.dst_pitch | (uintptr_t)g.row_bytes;
-      // 2: 32-byte rows (256-bit loads / stores), 1: 16-byte rows, 0: 2-byte granules
-      g.vec = (al & 31) == 0 ? 2 : (al & 15) == 0 ? 1 : 0;
+      // 2: 32-byte rows (256-bit loads / stores), 1: 16-byte rows, 0: 2-byte granules.
+      // The 256-bit path is used only for sources in this device's own memory
+      // (measured here); peer / IPC-mapped sources (NVLink) keep 16-byte loads.
+      bool local_src = false;
+      cudaPointerAttributes pa = {};
+      if (cudaPointerGetAttributes(&pa, g.src) == cudaSuccess)
+        local_src = pa.type == cudaMemoryTypeDevice && pa.device == device;
+      cudaGetLastError();
+      g.vec = ((al & 31) == 0 && local_src) ? 2 : (al & 15) == 0 ? 1 : 0;
     }
     chunks += g.nchunks;
   }
