@@ -65,7 +65,15 @@ namespace gemm {
 
 constexpr int BM = 128;       // rows per CTA (UMMA M = BM * CG)
 constexpr int UMMA_N = 256;   // columns per tcgen05.mma (one accumulator)
-constexpr int BK = 64;        // k per stage (one 128-byte swizzle row of bf16)
+// k per stage: 64 (A rows are one 128-byte swizzle row of bf16, SWIZZLE_128B)
+// or 32 (A rows 64 bytes, SWIZZLE_64B; twice the stages in the same smem)
+#ifndef UM_BK
+#define UM_BK 64
+#endif
+constexpr int BK = UM_BK;
+static_assert(BK == 64 || BK == 32, "BK is 64 or 32");
+constexpr int A_SW_BYTES = BK * 2;            // A's swizzle span: one row of the stage's A tile
+constexpr uint32_t A_LAYOUT = BK == 64 ? 2u : 4u;   // UMMA smem layout: SWIZZLE_128B / SWIZZLE_64B
 constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
 // epilogue warps: 4 (each drains a 32-lane quarter of TMEM, 2 smem boxes) or
 // 8 (two warps per quarter, each owning half the columns; the warp loads its
@@ -92,7 +100,7 @@ struct Cfg {
   static constexpr int EPI_BOXES = EW == 4 ? 2 : 1;           // smem boxes per epilogue warp
   static constexpr int NACC = NT / UMMA_N;                   // accumulators per tile
   static constexpr int NBUF = 2 / NACC;                      // TMEM tile buffers
-  static constexpr int STAGES = (CG == 2 && NT == 256) ? 6 : 4;
+  static constexpr int STAGES = ((CG == 2 && NT == 256) ? 6 : 4) * (64 / BK);
   static constexpr int SUB_PER_ACC = UMMA_N / CG / 64;       // 64-col B sub-tiles per accumulator per CTA
   static constexpr int B_SUBS = NACC * SUB_PER_ACC;
   static constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
@@ -735,7 +743,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const uint32_t sa = ptx::smem_u32(smem_a + stg * C::A_BYTES);
         const uint32_t sb = ptx::smem_u32(smem_b + stg * C::B_BYTES) + j * C::SUB_PER_ACC * SUB_BYTES;
 #if UM_PROFILE
-        if (works[0].debug_mma == 2) {   // (profiling) B read as K-major SW128: UMMA rate vs operand major-ness
+        if (BK == 64 && works[0].debug_mma == 2) {   // (profiling) B read as K-major SW128: UMMA rate vs operand major-ness
           constexpr uint32_t idesc_k = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 0);
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {
@@ -748,8 +756,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
 #endif
 #pragma unroll
         for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-          // A: K-major SW128, 8-row groups 1024 B apart; advance 32 B per UMMA_K.
-          const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
+          // A: K-major, swizzled rows of BK bf16; 8-row groups 8 * A_SW_BYTES apart;
+          // advance 32 B per UMMA_K inside the swizzle row.
+          const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 8 * A_SW_BYTES, A_LAYOUT);
           // B: MN-major SW128; 64-column blocks SUB_BYTES apart (LBO), 8-k groups
           // 1024 B apart (SBO); advance 16 k-rows = 2048 B per UMMA_K.
           const uint64_t bdesc = ptx::make_smem_desc(sb + kk * (UMMA_K * 128), SUB_BYTES, 1024);
@@ -1176,7 +1185,8 @@ static CUtensorMapL2promotion l2_promotion() {
   }
 }
 
-static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint32_t box_rows, const char* what) {
+static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint32_t box_rows, const char* what,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return fail(UM_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const CUtensorMapDataType dt = v.dtype == UM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -1185,7 +1195,7 @@ static int encode_2d(CUtensorMap* map, const um_view& v, uint32_t box_cols, uint
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, v.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swz, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(UM_ECUDA, std::string("cuTensorMapEncodeTiled failed for ") + what + " (code " +
                               std::to_string((int)r) + ")");
@@ -1648,7 +1658,9 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     if (op.done_flag)
       w.slot = (int)(std::find(slot_flags.begin(), slot_flags.end(), op.done_flag) - slot_flags.begin());
     CUtensorMap ma, mbm, mc;
-    if ((rc = encode_2d(&ma, op.a, BK, BM, "A")) || (rc = encode_2d(&mbm, op.b, 64, BK, "B"))) return rc;
+    if ((rc = encode_2d(&ma, op.a, BK, BM, "A", BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)) ||
+        (rc = encode_2d(&mbm, op.b, 64, BK, "B")))
+      return rc;
     if (!op.c_remote) {
       if ((rc = encode_2d(&mc, op.c, 32, 32, "C"))) return rc;
     } else {
