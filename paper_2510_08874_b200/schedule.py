@@ -199,14 +199,19 @@ def plan_bands(s: DirectSchedule, in_kernel: list, cfg: ExecConfig, row_cuts: di
             raster = False
             if len(nc) == 2 and _RASTER_N and nlen >= 2 * _RASTER_N and len(cuts_i) > 2:
                 # B read in place: cut n into _RASTER_N-wide pieces and walk the
-                # row slices piece by piece, so the launch runs like one op in
-                # K1's raster (a few n-tiles of B hot in L2 over the m sweep)
-                # instead of every row slice streaming all of B
+                # row slices piece by piece inside groups of a quarter of the
+                # slices, so the launch runs like K1's raster (a few n-tiles of
+                # B hot in L2 over the group's rows) while the row slices still
+                # complete -- and their replica reductions start -- in four
+                # waves over the launch instead of all at its end
                 nc = list(range(0, nlen, _RASTER_N)) + [nlen]
                 raster = True
             R, Cn = len(cuts_i) - 1, len(nc) - 1
-            cells = ([(t, b_) for b_ in range(Cn) for t in range(R)] if raster
-                     else [(t, b_) for t in range(R) for b_ in range(Cn)])
+            if raster:
+                G = max(1, R // 4)
+                cells = [(t, b_) for g0 in range(0, R, G) for b_ in range(Cn) for t in range(g0, min(R, g0 + G))]
+            else:
+                cells = [(t, b_) for t in range(R) for b_ in range(Cn)]
             for t, b_ in cells:
                 items.append((i, t * Cn + b_, cuts_i[t], cuts_i[t + 1], nc[b_], nc[b_ + 1], 0, klen))
             continue
