@@ -58,3 +58,30 @@ def test_sub_slices_reducers_and_expected_signals(case, panels):
             assert r0 <= lo + m0 and lo + m1 <= r1            # an item never straddles two sub-slices
             signalled[key] = signalled.get(key, 0) + 1
     assert signalled == {k_: v for k_, v in ovl.expected.items() if v}
+
+
+def test_row_sliced_op_raster_order():
+    """cfg3 at p = 8: each rank's 8192^3 op, cut at the reducers' row
+    sub-slices, is also cut into 2048-column pieces and walked piece-major
+    inside four groups of row slices: the pieces tile the op exactly once,
+    and the row-slice groups complete one after the other."""
+    from paper_2510_08874_b200 import schedule as sch
+
+    A, B, C = problem(8192, 8192, 65536, 8, "col", "row", "2d", 1, 1, 8)
+    cfg = ExecConfig(reduce_panels=4)
+    ovl = rt._ReduceOverlap(A, B, C, cfg)
+    sched = rt.lower_direct(A, B, C, cfg, 0)
+    sig = ovl.signals_for(sched)
+    items, _, _ = rt.plan_bands(sched, [True] * len(sched.fetches), cfg, {i: c for i, (c, _) in sig.items()})
+    op = sched.ops[0]
+    mlen, nlen = len(op.m_bound), len(op.n_bound)
+    cells = [(m0, m1, n0, n1) for (_, _, m0, m1, n0, n1, _, _) in items]
+    assert sum((m1 - m0) * (n1 - n0) for m0, m1, n0, n1 in cells) == mlen * nlen
+    assert len(set(cells)) == len(cells)
+    assert {n1 - n0 for _, _, n0, n1 in cells} == {sch._RASTER_N}
+    rows = sorted({(m0, m1) for m0, m1, _, _ in cells})
+    group = {r: g * 4 // len(rows) for g, r in enumerate(rows)}       # quarter of the row slices
+    seq = [group[(m0, m1)] for m0, m1, _, _ in cells]
+    assert seq == sorted(seq)                                          # groups in order
+    first = cells[: len(rows) // 4]
+    assert len({(n0, n1) for _, _, n0, n1 in first}) == 1              # piece-major inside a group
