@@ -74,6 +74,9 @@ PROF_ONLY = ("UM_GEMM_PAIRS", "UM_GEMM_EPI_WARPS", "UM_GEMM_CG", "UM_GEMM_EPI_DE
     {"UM_GEMM_TAIL_SPLIT": "1"},                         # last wave split along k (fused launches, gets)
     {"UM_GEMM_SKSTART": "0"},                            # no staggered start
     {"UM_GEMM_CG": "1"},                                 # cta_group::1 (profiling build)
+    {"UM_GEMM_PDL": "0"},                                # without programmatic dependent launch
+    {"UM_GEMM_SPLITK": "0"},                             # small launches without split-k
+    {"UM_RASTER_N": "0"},                                # row-sliced ops walked row-major
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_variant_exact(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
