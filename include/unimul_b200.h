@@ -179,7 +179,7 @@ UM_API int um_gemm_acc(const um_view* a, const um_view* b, const um_view* c, voi
 UM_API int um_gemm_acc_batch(const um_gemm_op* ops, int32_t nops, int32_t device, void* stream);
 
 /* Fused get -> GEMM: ONE persistent launch that pulls `gets` with dedicated
- * get warps on every SM (chunks handed out in list order) while the tensor
+ * get warps on every SM (chunks handed out in the order the launch first needs each get) while the tensor
  * cores run the ops; an op whose get_mask names pulls starts loading
  * only after every chunk of that pull has landed (device-side acquire), so
  * the reference's ordering rule "a compute depends on completion of its input

@@ -54,6 +54,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <queue>
 #include <vector>
 
 #include "um_internal.h"
@@ -297,6 +298,7 @@ struct alignas(64) LaunchArgs {
   CUtensorMap inl_maps[3 * MAX_INLINE_OPS];
   Work inl_works[MAX_INLINE_OPS];
   GetDesc gets[MAX_GETS];
+  int32_t get_order[MAX_GETS];  // pull order: the i-th get pulled is gets[get_order[i]] (chunk_start ascending)
 };
 static_assert(sizeof(LaunchArgs) <= 32764, "kernel parameter block");
 
@@ -1037,7 +1039,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     // ===================== get engine (GET_WARPS warps per CTA) =====================
     // Pulls the launch's remote operand slices into local staging buffers while
     // the tensor cores work on ops whose operands are already here.  Chunks are
-    // handed out in get order from a global counter, so every resident CTA
+    // handed out in pull order (get_order: first need) from a global counter, so every resident CTA
     // helps and the first ops' operands land first.  No wait on anything but its
     // own loads: deadlock-free whatever the SMs are doing.
     int* const chunk_ctr = &args.counters[2];
@@ -1054,8 +1056,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const uint64_t due = t_begin + (uint64_t)c * args.get_ns_per_chunk;
         while (ptx::globaltimer() < due) __nanosleep(200);
       }
-      int j = 0;
-      while (j + 1 < args.ngets && args.gets[j + 1].chunk_start <= c) ++j;
+      int oi = 0;
+      while (oi + 1 < args.ngets && args.gets[args.get_order[oi + 1]].chunk_start <= c) ++oi;
+      const int j = args.get_order[oi];
       const GetDesc& g = args.gets[j];
       const int r0 = (c - g.chunk_start) * g.rows_per_chunk;
       const int r1 = min(g.rows, r0 + g.rows_per_chunk);
@@ -1217,6 +1220,7 @@ struct Knobs {
   int chain = 1;
   int chain_waves = 6;
   int pdl = 1;
+  int pull_order = 1;
   int tail_split = 0;
   int cpf = 0;
   int stagger = 0;
@@ -1253,6 +1257,7 @@ static const Knobs& knobs() {
     k.chain = env_int("UM_GEMM_CHAIN", 1) ? 1 : 0;
     k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
     k.pdl = env_int("UM_GEMM_PDL", 1) ? 1 : 0;
+    k.pull_order = env_int("UM_GEMM_PULL_ORDER", 1) ? 1 : 0;
     k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
@@ -1825,6 +1830,43 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   }
   for (int s = 0; s < args.nslots; ++s) args.slots[s] = {slot_flags[s], slot_expected[s], slot_inc[s]};
   // ---- in-kernel gets (fused K2)
+  // Pull order: by the time the launch first needs each get.  The tiles are
+  // list-scheduled on the CTA pairs in work order with no waits (a segment's
+  // time ~ its k-blocks); a get's need time is the earliest start of a
+  // segment that waits on it.  The first-use order of the work list would
+  // pull the second segments of the first wave's tiles before the first
+  // segments of later first-wave tiles (UM_GEMM_PULL_ORDER=0 keeps it).
+  std::vector<int> gorder(std::max(0, ngets));
+  for (int i = 0; i < ngets; ++i) gorder[i] = i;
+  if (ngets > 1 && kn.pull_order) {
+    std::vector<double> need_t(ngets, 1e300);
+    int pairs = 148;
+    cudaDeviceGetAttribute(&pairs, cudaDevAttrMultiProcessorCount, device);
+    pairs = std::max(1, pairs / CG);
+    if (grid_limit(device) > 0) pairs = std::max(1, std::min(pairs, grid_limit(device)));
+    std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+    for (int q = 0; q < pairs; ++q) free_at.push(0.0);
+    for (size_t h = 0; h < works.size(); ++h) {
+      if (works[h].nseg <= 0) continue;
+      const long ntiles = (long)works[h].tiles_m * works[h].tiles_n;
+      for (long tl = 0; tl < ntiles; ++tl) {
+        double tt = free_at.top();
+        free_at.pop();
+        for (size_t w = h; w < h + (size_t)works[h].nseg && w < works.size(); ++w) {
+          const Work& x = works[w];
+          auto use = [&](int g) { if (g >= 0 && g < ngets) need_t[g] = std::min(need_t[g], tt); };
+          use(x.a_fine - 1);
+          use(x.b_fine - 1);
+          for (int g = 0; g < ngets && g < 64; ++g)
+            if ((x.wait_mask >> g) & 1ull) use(g);
+          tt += (double)std::max(1, x.seg_kb);
+        }
+        free_at.push(tt);
+      }
+    }
+    std::stable_sort(gorder.begin(), gorder.end(), [&](int a, int b) { return need_t[a] < need_t[b]; });
+  }
+  for (int i = 0; i < ngets; ++i) args.get_order[i] = gorder[i];
   int chunks = 0;
   for (int i = 0; i < ngets; ++i) {
     const um_get_desc& gd = gets_in[i];
@@ -1844,7 +1886,6 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
     g.row_bytes = (int32_t)(view_cols(gd.src) * es);
     g.rows_per_chunk = std::max(1, GET_CHUNK_BYTES / std::max(1, g.row_bytes));
     g.nchunks = g.rows && g.row_bytes ? (g.rows + g.rows_per_chunk - 1) / g.rows_per_chunk : 0;
-    g.chunk_start = chunks;
     g.row0 = (int32_t)gd.dst.row_lo;
     {
       const uintptr_t al = reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst) |
@@ -1859,6 +1900,10 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
       cudaGetLastError();
       g.vec = ((al & 31) == 0 && local_src) ? 2 : (al & 15) == 0 ? 1 : 0;
     }
+  }
+  for (int oi = 0; oi < ngets; ++oi) {   // chunk ranges in pull order
+    GetDesc& g = args.gets[gorder[oi]];
+    g.chunk_start = chunks;
     chunks += g.nchunks;
   }
   args.ngets = ngets;
