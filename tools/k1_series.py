@@ -3,7 +3,9 @@ one shape, with the SM clock sampled by NVML between blocks: tells a
 power-cap clock drop (times drift up with the clock going down) from a
 scheduling effect (bimodal launch times at a steady clock).
 
-    python tools/k1_series.py [--shape 8192x8192x8192] [--iters 40] [--blocks 4] [--env K=V,...]
+    python tools/k1_series.py [--shape 8192x8192x8192] [--iters 40] [--blocks 4] [--impls k1,lt]
+
+(the clock probe is tools/debug/clk_probe.so: make -C tools/debug)
 """
 import argparse
 import ctypes
