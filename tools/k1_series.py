@@ -1,7 +1,8 @@
 """Per-launch time series of K1 vs cuBLASLt (bf16 x bf16 -> fp32, beta = 1) on
-one shape, with the SM clock sampled by NVML between blocks: tells a
-power-cap clock drop (times drift up with the clock going down) from a
-scheduling effect (bimodal launch times at a steady clock).
+one shape, with the SM clock the kernels actually ran at (a one-warp
+clock64 / globaltimer sampler co-resident with the GEMM: `kernel_mhz`) and
+NVML's view (`sm_mhz`, `watts`).  TFLOP/s per GHz separates kernel
+efficiency from the power cap.
 
     python tools/k1_series.py [--shape 8192x8192x8192] [--iters 40] [--blocks 4] [--impls k1,lt]
 
