@@ -90,8 +90,8 @@ class _RankRun:
         self.done = None
         self.signals = None        # op -> (row cuts, (m0, m1) -> done_flag): overlapped replica reduction
         self.signals_key = None
-        for ev in start_events:
-            self.gs.wait_event(ev)
+        self.start_events = list(start_events)
+        for ev in self.start_events:   # the get stream waits only if the plan uses it (_replay)
             self.cs.wait_event(ev)
 
     def _mat(self, name):
@@ -501,6 +501,12 @@ class _RankRun:
         with torch.cuda.device(self.dev):
             events = {}
             gsp = ctypes.c_void_p(self.gs.cuda_stream)
+            # the get stream carries copy-engine pulls only; a plan without
+            # them (every pull in-kernel, or none) neither forks nor joins it
+            uses_gs = bool(plan.host_fetches) or bool(plan.flagged)
+            if uses_gs:
+                for ev in self.start_events:
+                    self.gs.wait_event(ev)
             if plan.flagged:
                 # reset the arrival flag before this run's K1 can read it
                 fptr = ctypes.c_void_p(plan.flag.data_ptr())
@@ -535,11 +541,12 @@ class _RankRun:
                     self._scratch_gemm(*act[1:])
             for j in plan.final_waits:
                 self.cs.wait_event(events[j])
-            # join the get stream back even when it carried nothing (keeps the
-            # multiply capturable into a CUDA graph: no unjoined forked stream)
-            ev = torch.cuda.Event()
-            ev.record(self.gs)
-            self.cs.wait_event(ev)
+            if uses_gs:
+                # join the get stream back (a multiply stays capturable into a
+                # CUDA graph: no unjoined forked stream)
+                ev = torch.cuda.Event()
+                ev.record(self.gs)
+                self.cs.wait_event(ev)
             self.done = torch.cuda.Event()
             self.done.record(self.cs)
         fab.counters.merge(plan.traffic)
