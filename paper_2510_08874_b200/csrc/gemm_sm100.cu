@@ -39,7 +39,8 @@
 //    512 (two N=256 accumulators filling TMEM: 25% fewer operand bytes per
 //    flop through L2; the MMA issuer runs the first k-blocks of a tile on
 //    accumulator 0 while the epilogue still drains accumulator 1, so most of
-//    the drain stays hidden).
+//    the drain stays hidden), or 128 for latency-bound launches with few tiles
+//    (one N=128 accumulator: half the per-SM drain, twice the SMs).
 //  * epilogue: tcgen05.ld -> registers -> swizzled smem -> TMA reduce-add
 //    (cp.reduce.async.bulk.tensor ... add) into the local C tile, or
 //    red.global.add.v4.f32 straight into a peer C tile (fused K3).
@@ -65,7 +66,7 @@ namespace um {
 namespace gemm {
 
 constexpr int BM = 128;       // rows per CTA (UMMA M = BM * CG)
-constexpr int UMMA_N = 256;   // columns per tcgen05.mma (one accumulator)
+constexpr int UMMA_N = 256;   // columns per tcgen05.mma (one accumulator), NT = 128: 128
 // k per stage: 64 (A rows are one 128-byte swizzle row of bf16, SWIZZLE_128B)
 // or 32 (A rows 64 bytes, SWIZZLE_64B; twice the stages in the same smem)
 #ifndef UM_BK
@@ -93,16 +94,22 @@ constexpr int num_threads(int ew, int gw) { return 64 + ew * 32 + gw * 32; }
 constexpr int GROUP_M = -4;
 constexpr int EPI_BOX_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32
 constexpr int SUB_BYTES = BK * 128;          // one 64-column B sub-tile of a stage (8 KiB)
+// launches of at most SMEM_WORKS works whose list sits in the parameter block
+// copy it into shared memory during setup (before the programmatic-launch
+// wait: kernel parameters are immutable), so no role's first tile waits on a
+// chain of dependent parameter-block loads
+constexpr int SMEM_WORKS = 8;
 
 template <int CG, int NT, int EW = 4, int GW = GET_WARPS>
 struct Cfg {
   static constexpr int EPI_WARPS = EW;
   static constexpr int NUM_THREADS = num_threads(EW, GW);
   static constexpr int EPI_BOXES = EW == 4 ? 2 : 1;           // smem boxes per epilogue warp
-  static constexpr int NACC = NT / UMMA_N;                   // accumulators per tile
+  static constexpr int UN = NT < UMMA_N ? NT : UMMA_N;       // columns per tcgen05.mma
+  static constexpr int NACC = NT / UN;                       // accumulators per tile
   static constexpr int NBUF = 2 / NACC;                      // TMEM tile buffers
-  static constexpr int STAGES = ((CG == 2 && NT == 256) ? 6 : 4) * (64 / BK);
-  static constexpr int SUB_PER_ACC = UMMA_N / CG / 64;       // 64-col B sub-tiles per accumulator per CTA
+  static constexpr int STAGES = ((CG == 2 && NT == 256) ? 6 : (CG == 2 && NT == 128) ? 8 : 4) * (64 / BK);
+  static constexpr int SUB_PER_ACC = UN / CG / 64;           // 64-col B sub-tiles per accumulator per CTA
   static constexpr int B_SUBS = NACC * SUB_PER_ACC;
   static constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
   static constexpr int B_BYTES = B_SUBS * SUB_BYTES;
@@ -113,12 +120,13 @@ struct Cfg {
 #else
   static constexpr int BAR_BYTES = 256;
 #endif
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  static constexpr int WORKS_BYTES = SMEM_WORKS * 160;       // first works copied at setup (sizeof(Work) == 160)
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES + WORKS_BYTES;
   static constexpr uint32_t TMEM_COLS = 512;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-struct alignas(16) Work {   // sizeof is a multiple of 16 (setup touches it as uint4)
+struct alignas(16) Work {   // sizeof is a multiple of 16 (setup copies it as uint4)
   int32_t m, n, k;
   int32_t tiles_m, tiles_n, num_kb;
   int32_t tile_start, c_remote;
@@ -142,6 +150,7 @@ struct alignas(16) Work {   // sizeof is a multiple of 16 (setup touches it as u
   int32_t debug_halfb;          // profiling only: skip half of the B loads (wrong results)
   int32_t debug_mma;            // profiling only: 1 = no operand loads (MMAs on stale smem), 2 = also B as K-major
 };
+static_assert(sizeof(Work) == 160, "Work layout (Cfg::WORKS_BYTES)");
 
 // One slice pull of the in-kernel get engine: rows x row_bytes from src (local,
 // peer or IPC-mapped memory) into a local staging buffer, cut into chunks of
@@ -291,6 +300,7 @@ struct alignas(64) LaunchArgs {
   int stag_ok;                // host: this launch may use a staggered start (set at prepare)
   int ext_waits;              // host: some op waits on an external arrival flag (copy-engine pull)
   int nsplit;                 // split-k pieces per tile (small launches), 1 = off
+  int smem_works;             // host: the work list (inline, <= SMEM_WORKS works) is read from a shared-memory copy
   uint32_t get_ns_per_chunk;  // > 0: pace the pulls to one chunk per this many ns (link-rate emulation)
   unsigned long long* prof;   // (profiling, UM_GEMM_STALLS) per cluster: MMA-thread cycles total / waiting
                               // for operands / for the epilogue to free TMEM / for the next tile
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   constexpr int CS = CG * NP;   // cluster size
   // small op lists travel inside the kernel parameters (no per-launch device
   // allocation or host->device copy); larger ones in a global-memory block
-  const Work* __restrict__ works = args.works ? args.works : args.inl_works;
+  const Work* __restrict__ works = args.works ? args.works : args.inl_works;   // (shared-memory copy below)
   const CUtensorMap* __restrict__ maps = args.maps ? args.maps : args.inl_maps;
   const int nwork = args.nwork;
   const int total_tiles = args.total_tiles;
@@ -336,6 +346,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   uint64_t* tq_full = bars + 2 * C::STAGES + 5;     // [TQ]
   uint64_t* tq_empty = tq_full + TQ;                // [TQ] (leader CTA)
   volatile int* tq = reinterpret_cast<volatile int*>(tq_empty + TQ);  // [TQ]
+  Work* smem_wk = reinterpret_cast<Work*>(reinterpret_cast<uint8_t*>(bars) + C::BAR_BYTES);   // [SMEM_WORKS]
 #if UM_PROFILE
   // (profiling) clock64 at which the leader's producer issued each stage's loads
   volatile unsigned long long* issue_ts = reinterpret_cast<volatile unsigned long long*>(tq_empty + TQ + TQ / 2);
@@ -402,11 +413,17 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     else ptx::mbar_arrive_cluster(&tq_empty[slot], 0);
     return t;
   };
+  if (args.smem_works && threadIdx.x >= 64) {
+    const int v = threadIdx.x - 64;
+    if (v < nwork * (int)(sizeof(Work) / 16))
+      reinterpret_cast<uint4*>(smem_wk)[v] = reinterpret_cast<const uint4*>(args.inl_works)[v];
+  }
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (args.smem_works) works = smem_wk;
   // Programmatic dependent launch: the setup above touches only this CTA's
   // shared memory and TMEM, so it may overlap the previous kernel's tail on
   // the stream (launched with programmatic stream serialization); every
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   // through a chain of dependent scalar loads, each a cold miss (~1 us) when
   // the work list sits in the parameter block; one parallel touch here (32
   // lanes x 16 B) brings them into the SM's caches during setup
-  if (warp == 2 || warp == 3) {
+  if (!args.smem_works && (warp == 2 || warp == 3)) {
     const int nvec = min(nwork, 8) * (int)(sizeof(Work) / 16);
     const int v = (warp - 2) * 32 + lane;
     if (v < nvec) {
@@ -581,7 +598,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const CUtensorMap* mbm = &maps[3 * w + 1];
         const uint64_t pa = pols[wk.a_pol], pb = pols[wk.b_pol];
         const int arow = wk.a_row0 + mb * BM * CG * NP + row_off;
-        const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (UMMA_N / CG);
+        const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (C::UN / CG);
         if (a_fine && lane == 0) wait_rows(a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
         __syncwarp();
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
@@ -593,7 +610,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           for (int j = 0; j < C::NACC; ++j)
 #pragma unroll
             for (int s = 0; s < C::SUB_PER_ACC; ++s)
-              ptx::tma_prefetch_2d(mbm, bcol + j * UMMA_N + s * 64, b_row0 + kb * BK);
+              ptx::tma_prefetch_2d(mbm, bcol + j * C::UN + s * 64, b_row0 + kb * BK);
         };
         const int pf = wk.prefetch;
         // k-blocks of this segment; a staggered or split-k unit (single-segment
@@ -662,7 +679,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
                 if (halfb && j == 1) continue;
                 const int qsub = j * C::SUB_PER_ACC + s;
                 const uint32_t dst = sb + qsub * SUB_BYTES;
-                const int col = bcol + j * UMMA_N + s * 64;
+                const int col = bcol + j * C::UN + s * 64;
                 if (mcast) {
                   // the CTAs with this pair rank in the other pairs need the same B
                   // sub-tiles: each loads 1/NP of them into all (multicast)
@@ -697,7 +714,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     // every operand of tcgen05.mma is warp-uniform; one elected lane issues.
     if (leader) {
       const bool issuer = ptx::elect_one();
-      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 1);
+      constexpr uint32_t idesc = ptx::make_idesc_bf16(BM * CG, C::UN, 0, 1);
       // a stage is free once every pair sharing its B (multicast) has consumed it
       const uint16_t EMPTY_MASK = (uint16_t)((1u << cs) - 1);
       const uint16_t PAIR_MASK = (uint16_t)(0x3u << (pair * CG));
@@ -746,7 +763,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const uint32_t sb = ptx::smem_u32(smem_b + stg * C::B_BYTES) + j * C::SUB_PER_ACC * SUB_BYTES;
 #if UM_PROFILE
         if (BK == 64 && works[0].debug_mma == 2) {   // (profiling) B read as K-major SW128: UMMA rate vs operand major-ness
-          constexpr uint32_t idesc_k = ptx::make_idesc_bf16(BM * CG, UMMA_N, 0, 0);
+          constexpr uint32_t idesc_k = ptx::make_idesc_bf16(BM * CG, C::UN, 0, 0);
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {
             const uint64_t adesc = ptx::make_smem_desc(sa + kk * (UMMA_K * 2), 16, 1024);
@@ -793,7 +810,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             wait_full(stage, phase);
             if (it == 0 && kb == 0 && lane == 0) stamp(4);
             ptx::tc_fence_after();
-            issue(stage, buf * UMMA_N, 0, kb == 0);
+            issue(stage, buf * C::UN, 0, kb == 0);
             if (issuer) ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
@@ -815,7 +832,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           ptx::tc_fence_after();
           int st = stage0;
           for (int kb = 0; kb < D; ++kb) {
-            issue(st, UMMA_N, 1, kb == 0);
+            issue(st, C::UN, 1, kb == 0);
             if (issuer) ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
@@ -826,7 +843,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
             wait_full(stage, phase);
             ptx::tc_fence_after();
             issue(stage, 0, 0, kb == 0);          // kb == 0 only without a leading stagger (D == 0)
-            issue(stage, UMMA_N, 1, kb == 0);
+            issue(stage, C::UN, 1, kb == 0);
             if (issuer) ptx::umma_commit<CG>(&empty[stage], EMPTY_MASK);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
@@ -840,7 +857,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           if (issuer) ptx::umma_commit<CG>(&tmem_full[0], PAIR_MASK);
           st = stageE;
           for (int kb = num_kb - E; kb < num_kb; ++kb) {
-            issue(st, UMMA_N, 1, false);
+            issue(st, C::UN, 1, false);
             if (issuer) ptx::umma_commit<CG>(&empty[st], EMPTY_MASK);
             if (++st == C::STAGES) st = 0;
           }
@@ -872,7 +889,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     // ===================== Epilogue (EW warps) =====================
     const int e = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access (hardware: warp % 4)
-    constexpr int CHUNKS = UMMA_N / 32;                       // 32-column chunks per accumulator
+    constexpr int CHUNKS = C::UN / 32;                       // 32-column chunks per accumulator
     constexpr int WCH = EW == 4 ? CHUNKS : CHUNKS / 2;        // chunks per warp per accumulator
     const int ch0 = EW == 4 ? 0 : (e / 4) * WCH;              // EW == 8: column half of this warp
     const uint64_t cpols[3] = {ptx::policy_evict_normal(), ptx::policy_evict_first(), ptx::policy_evict_last()};
@@ -993,9 +1010,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         ptx::mbar_wait(&tmem_full[C::NACC == 1 ? buf : j], tph);
         if (it == 0 && j == 0 && e == 0 && lane == 0) stamp(6);
         ptx::tc_fence_after();
-        const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * UMMA_N;
+        const uint32_t acc_col = (uint32_t)(buf * C::NACC + j) * C::UN;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc_col;
-        const int col_acc = nb * NT + j * UMMA_N;
+        const int col_acc = nb * NT + j * C::UN;
         if constexpr (EW == 8) {
           // whole 128-column share in registers, TMEM released before any reduce
           uint32_t r[WCH][32];
@@ -1210,7 +1227,7 @@ static int env_int(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-// Tuning knobs (read once): UM_GEMM_CG=1|2, UM_GEMM_NT=256|512 (0 = auto),
+// Tuning knobs (read once): UM_GEMM_CG=1|2, UM_GEMM_NT=128|256|512 (0 = auto),
 // UM_GEMM_GROUP=<m-tiles, negative: n-tiles>, UM_GEMM_APOL / UM_GEMM_BPOL
 // = 0 normal | 1 evict_first | 2 evict_last (-1 = auto).
 struct Knobs {
@@ -1226,6 +1243,7 @@ struct Knobs {
   int stagger = 0;
   int skstart = 1;
   int splitk = 1;
+  int smem_works = 1;   // short inline work lists read from a shared-memory copy (UM_GEMM_SMEM_WORKS=0: off)
 };
 static const Knobs& knobs() {
   static Knobs k;
@@ -1263,6 +1281,7 @@ static const Knobs& knobs() {
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
     k.skstart = env_int("UM_GEMM_SKSTART", 1) ? 1 : 0;
     k.splitk = env_int("UM_GEMM_SPLITK", 1) ? 1 : 0;
+    k.smem_works = env_int("UM_GEMM_SMEM_WORKS", 1) ? 1 : 0;
   });
   return k;
 }
@@ -1428,7 +1447,7 @@ static void pick_variant(const std::vector<um_gemm_op>& ops, int sms, int& cg, i
     nt = 256;
     return;
   }
-  if (kn.nt == 256 || kn.nt == 512) {
+  if (kn.nt == 128 || kn.nt == 256 || kn.nt == 512) {
     nt = kn.nt;
     return;
   }
@@ -1454,9 +1473,13 @@ static void pick_variant(const std::vector<um_gemm_op>& ops, int sms, int& cg, i
   }
   // the wider tile moves ~25 % fewer operand bytes per flop and measured 7-14 %
   // faster per tile; only when there are too few tiles for two waves does the
-  // narrower one win (measured: cfg5 p=8's 256 tiles still run best at 512)
-  (void)t256;
-  nt = t512 >= 2 * (int64_t)std::max(1, sms / 2) ? 512 : 256;
+  // narrower one win (measured: cfg5 p=8's 256 tiles still run best at 512).
+  // A launch whose 256-wide tiles fill at most half the pairs is latency
+  // bound, and its tail is the drain of each CTA's fp32 accumulator (one SM
+  // moves ~25-45 B/clk of it into C, tools/debug/drain_probe.cu): 128-wide
+  // tiles halve the drain per SM and spread it over twice the SMs
+  const int64_t pairs = std::max(1, sms / 2);
+  nt = t512 >= 2 * pairs ? 512 : (2 * t256 <= pairs ? 128 : 256);
 }
 
 // A launch with everything host-side resolved: tensor maps encoded, work
@@ -1552,7 +1575,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   const Knobs& kn = knobs();
   P->CG = CG;
   P->NT = NT;
-  P->EW = (CG == 2 && kn.epi_warps == 8) ? 8 : 4;
+  P->EW = (CG == 2 && kn.epi_warps == 8 && NT != 128) ? 8 : 4;
   // experimental: clusters of 2 pairs sharing B by TMA multicast (UM_GEMM_PAIRS=2)
   P->NP = (CG == 2 && NT == 512 && P->EW == 4) ? kn.pairs : 1;
   const int NPAIR = P->NP;
@@ -1581,7 +1604,7 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   }
   if ((int)slot_flags.size() > MAX_SLOTS)
     return fail(UM_EVALUE, "more than " + std::to_string(MAX_SLOTS) + " distinct done_flags in one launch");
-  const int epi_arrivals = (CG == 2 ? 2 : 1) * ((CG == 2 && kn.epi_warps == 8) ? 8 : 4) * NPAIR;
+  const int epi_arrivals = (CG == 2 ? 2 : 1) * P->EW * NPAIR;
   for (int i = 0; i < nops; ++i) {
     const um_gemm_op& op = ops[i];
     if (op.c_remote && op.c.dtype == UM_F32 && (reinterpret_cast<uintptr_t>(op.c.base) & 3))
@@ -1934,8 +1957,10 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   if (works.size() <= (size_t)MAX_INLINE_OPS && !maps_global) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
     memcpy(args.inl_works, works.data(), works.size() * sizeof(Work));
+    args.smem_works = knobs().smem_works && works.size() <= (size_t)SMEM_WORKS ? 1 : 0;
   } else {
     // large op lists: one stream-ordered allocation carries work list + tensor maps
+    args.smem_works = 0;
     const size_t maps_bytes = maps.size() * sizeof(CUtensorMap);
     const size_t works_bytes = works.size() * sizeof(Work);
     std::vector<uint8_t> host(maps_bytes + works_bytes);
@@ -1995,6 +2020,8 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
 #endif
   if (P->NT == 512)
     rc = g ? launch<2, 512, 4, GET_WARPS>(args, P->device, stream) : launch<2, 512, 4, 0>(args, P->device, stream);
+  else if (P->NT == 128)
+    rc = g ? launch<2, 128, 4, GET_WARPS>(args, P->device, stream) : launch<2, 128, 4, 0>(args, P->device, stream);
   else
     rc = g ? launch<2, 256, 4, GET_WARPS>(args, P->device, stream) : launch<2, 256, 4, 0>(args, P->device, stream);
   args.prof = nullptr;

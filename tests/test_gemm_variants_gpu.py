@@ -66,6 +66,7 @@ PROF_ONLY = ("UM_GEMM_PAIRS", "UM_GEMM_EPI_WARPS", "UM_GEMM_CG", "UM_GEMM_EPI_DE
     {"UM_GEMM_PAIRS": "4"},                              # preferred clusters of 8
     {"UM_GEMM_PAIRS": "4", "UM_GEMM_PAIRS_FIXED": "1"},  # clusters of 8 only
     {"UM_GEMM_NT": "256"},
+    {"UM_GEMM_NT": "128"},                               # narrow tiles everywhere (default: few-tile launches)
     {"UM_GEMM_EPI_WARPS": "8"},
     {"UM_GEMM_CHAIN_WAVES": "0"},                        # uncapped k-chains
     {"UM_GEMM_CHAIN": "0"},

@@ -17,7 +17,8 @@ def v(t, dt):
     return C.UmView(t.data_ptr(), 0, t.shape[0], 0, t.shape[1], t.stride(0), dt, 0)
 
 
-for s in (256, 1024, 2048, 4096):
+SIZES = [int(x) for x in os.environ.get("UM_PROBE_SIZES", "256,1024,2048,4096").split(",")]
+for s in SIZES:
     a = torch.randn(s, s, device="cuda").to(torch.bfloat16)
     b = torch.randn(s, s, device="cuda").to(torch.bfloat16)
     c = torch.zeros(s, s, device="cuda")
