@@ -534,12 +534,69 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     # of the concurrent pair
     bw = pcie_bandwidth(dev)
     floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
+    # the same copies in the order multiply_from_host issues them, each C block
+    # downloadable only once its A rows and B columns are up (and computed at
+    # the measured peak): the floor of this block pipeline, not only of PCIe
+    P = args.panels
+    Q = args.col_panels
+    if Q is None:
+        big_b = B.global_shape.rows * B.global_shape.cols * 4 >= m * k
+        Q = P if (big_b and C.c == 1) else 1
+    pipe_ms = pipeline_floor_ms(P, Q, nbytes(A), nbytes(B), d2h, flops, bw["h2d_concurrent_gbs"],
+                                bw["d2h_concurrent_gbs"], load_peaks()[0], bw["h2d_gbs"], bw["d2h_gbs"])
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
             "api": ("hostio.multiply_from_host" if (world > 1 or not args.e2e_graph)
                     else "hostio.CapturedHostMultiply (multiply_from_host as one CUDA graph)"),
             "panels": args.panels, "col_panels": args.col_panels, "copy_streams": args.copy_streams,
-            "roofline": {"bound": "pcie", "floor_ms_per_step": floor_ms, "frac": floor_ms / ms, **bw}}
+            "roofline": {"bound": "pcie", "floor_ms_per_step": floor_ms, "frac": floor_ms / ms,
+                         "pipeline_floor_ms_per_step": pipe_ms, "pipeline_frac": pipe_ms / ms,
+                         "pipeline_grid": [P, Q], **bw}}
+
+
+def pipeline_floor_ms(P: int, Q: int, a_bytes: int, b_bytes: int, c_bytes: int, flops: float, up_gbs: float,
+                      dn_gbs: float, peak_tflops: float, up_alone_gbs: float | None = None,
+                      dn_alone_gbs: float | None = None) -> float:
+    """Lower bound of hostio's block pipeline: uploads back to back on one
+    stream in the issue order (Q > 1: A row panel i / B column panel j the
+    first time a block of the shell order needs it; Q == 1: all of B, then A
+    row panels), each block computed at `peak_tflops` once its panels are up
+    and the previous block is done, and downloaded after that, back to back
+    on one stream.  Uploads run at the one-direction rate until the first
+    download starts, downloads at it once the uploads are done, both at the
+    concurrent rate in between.  C += A.B needs all of A's rows and B's
+    columns of a block before any of it is final, so even continuous square
+    shells cannot beat 1.25 x the PCIe floor."""
+    from paper_2510_08874_b200.hostio import _shell_order
+
+    up_alone = up_alone_gbs or up_gbs
+    dn_alone = dn_alone_gbs or dn_gbs
+    order = _shell_order(P, Q) if Q > 1 else [(i, 0) for i in range(P)]
+    # uploads in issue order: (bytes, panel key)
+    ups = [(b_bytes, ("b", 0))] if Q == 1 else []
+    seen = set(k for _, k in ups)
+    for i, j in order:
+        for key, nb in ((("a", i), a_bytes / P), (("b", j), b_bytes / Q)):
+            if key not in seen:
+                seen.add(key)
+                ups.append((nb, key))
+    first_dn = None
+    for _ in range(3):   # the first download's start and the upload times depend on each other
+        t_up, at = 0.0, {}
+        for nb, key in ups:
+            rate = up_alone if first_dn is None or t_up < first_dn else up_gbs
+            t_up += nb / (rate * 1e9) * 1e3
+            at[key] = t_up
+        t_c = t_d = 0.0
+        start = None
+        for i, j in order:
+            t_c = max(t_c, at[("a", i)], at[("b", j if Q > 1 else 0)]) + flops / (P * Q) / (peak_tflops * 1e12) * 1e3
+            s0 = max(t_d, t_c)
+            start = s0 if start is None else start
+            rate = dn_alone if s0 >= t_up else dn_gbs
+            t_d = s0 + c_bytes / (P * Q) / (rate * 1e9) * 1e3
+        first_dn = start
+    return t_d
 
 
 def pcie_bandwidth(dev, nbytes: int = 1 << 30, reps: int = 3) -> dict:

@@ -57,3 +57,22 @@ def test_default_workload_is_cfg5():
     assert 'add_argument("--config", default="cfg5"' in src
     m, n, k, ap, bp, cp, *_ = bench.CONFIGS["cfg5"]
     assert (m, n, k, ap, bp, cp) == (16384, 16384, 16384, "2d", "col", "row")
+
+
+def test_pipeline_floor_bounds():
+    """The e2e block-pipeline floor (bench.pipeline_floor_ms) sits between the
+    PCIe floor and the one-block pipeline, and a square shell grid beats
+    uploading B whole first (row panels)."""
+    import bench
+
+    G = 1 << 30
+    flops = 2 * 16384 ** 3
+    pcie = G / 50e9 * 1e3
+    grids = {(P, Q): bench.pipeline_floor_ms(P, Q, G // 2, G // 2, G, flops, 50.0, 50.0, 1600.0)
+             for P, Q in ((1, 1), (4, 4), (8, 8), (8, 1))}
+    for v in grids.values():
+        assert v >= 1.25 * pcie - 1e-6          # C blocks need whole A rows and B columns
+    assert grids[(1, 1)] >= 2 * pcie - 1e-6     # upload everything, then download everything
+    assert grids[(8, 8)] < grids[(4, 4)] < grids[(8, 1)] < grids[(1, 1)]
+    # faster one-direction copies only lower the floor
+    assert bench.pipeline_floor_ms(4, 4, G // 2, G // 2, G, flops, 50.0, 50.0, 1600.0, 56.0, 57.0) < grids[(4, 4)]
