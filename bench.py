@@ -504,7 +504,35 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     d2h = nbytes(C, replica0_only=True)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world == 1 and args.e2e_graph:
+    steps = max(1, args.steps // 2)
+    single_ms = None
+    if world == 1 and not args.e2e_graph and not args.e2e_single:
+        # the K steps as one multiply_from_host_many call: step s + 1's uploads
+        # overlap step s's download tail (every step still uploads its A and B
+        # and downloads its C); the one-call-per-step pipeline is timed too
+        from paper_2510_08874_b200.hostio import multiply_from_host_many
+
+        def run(n_jobs):
+            multiply_from_host_many(A, B, C, [(a_h, b_h, c_h)] * n_jobs, cfg, panels=args.panels,
+                                    col_panels=args.col_panels)
+
+        run(max(1, args.warmup))
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, col_panels=args.col_panels)
+        e1.record()
+        barrier()
+        single_ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+        e0.record()
+        run(steps)
+        e1.record()
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+        api = (f"hostio.multiply_from_host_many ({steps} jobs in one call: each job's uploads start once the "
+               f"previous job no longer reads the device panel, i.e. during its download tail)")
+    elif world == 1 and args.e2e_graph:
         # the host-streaming multiply replayed as one CUDA graph: every replay
         # still uploads A and B from the pinned host buffers and downloads C
         from paper_2510_08874_b200.hostio import CapturedHostMultiply
@@ -518,17 +546,19 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
             multiply_from_host(A, B, C, a_h, b_h, c_h, cfg, panels=args.panels, copy_streams=args.copy_streams,
                                col_panels=args.col_panels)
 
-    for _ in range(max(1, args.warmup)):
-        step()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    steps = max(1, args.steps // 2)
-    for _ in range(steps):
-        step()
-    e1.record()
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    if single_ms is None:
+        for _ in range(max(1, args.warmup)):
+            step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+        api = ("hostio.multiply_from_host" if (world > 1 or not args.e2e_graph)
+               else "hostio.CapturedHostMultiply (multiply_from_host as one CUDA graph)")
     # the e2e roofline: this box's pinned-memory copy bandwidth, each direction
     # alone and both at once (PCIe is full duplex); floor = the slower direction
     # of the concurrent pair
@@ -545,9 +575,8 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
     pipe_ms = pipeline_floor_ms(P, Q, nbytes(A), nbytes(B), d2h, flops, bw["h2d_concurrent_gbs"],
                                 bw["d2h_concurrent_gbs"], load_peaks()[0], bw["h2d_gbs"], bw["d2h_gbs"])
     return {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "api": ("hostio.multiply_from_host" if (world > 1 or not args.e2e_graph)
-                    else "hostio.CapturedHostMultiply (multiply_from_host as one CUDA graph)"),
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps, "api": api,
+            "single_call_ms_per_step": single_ms,
             "panels": args.panels, "col_panels": args.col_panels, "copy_streams": args.copy_streams,
             "roofline": {"bound": "pcie", "floor_ms_per_step": floor_ms, "frac": floor_ms / ms,
                          "pipeline_floor_ms_per_step": pipe_ms, "pipeline_frac": pipe_ms / ms,
@@ -648,6 +677,9 @@ def main():
                     help="column panels of the e2e block grid (default: hostio's choice)")
     ap.add_argument("--e2e-graph", action="store_true",
                     help="e2e through hostio.CapturedHostMultiply (the same copies + launches replayed as a CUDA graph)")
+    ap.add_argument("--e2e-single", action="store_true",
+                    help="e2e as one multiply_from_host call per step (default: the steps as one pipelined "
+                         "multiply_from_host_many call)")
     ap.add_argument("--copy-streams", type=int, default=1, help="copy streams per direction in the e2e path (measured: 1 best)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=10.0, help="target seconds of CPU oracle work")

@@ -203,12 +203,25 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
 @nvtx("um:multiply_from_host_blocks")
 def _multiply_blocks(A, B, C, a_host, b_host, c_out, cfg, P: int, Q: int, copy_streams: int) -> dict:
     """multiply_from_host over a P x Q block grid of C in shell order."""
+    return _multiply_blocks_jobs(A, B, C, [(a_host, b_host, c_out)], cfg, P, Q, copy_streams)
+
+
+def _multiply_blocks_jobs(A, B, C, jobs, cfg, P: int, Q: int, copy_streams: int) -> dict:
+    """One or more host-streaming multiplies over a P x Q block grid in shell
+    order, issued back to back.  Job s + 1 is ordered against job s block by
+    block instead of as a whole: its upload of A row panel i (B column panel j)
+    waits only for job s's last block that reads that panel, and its block
+    (i, j) computes only after job s's download of block (i, j).  So the next
+    job's uploads run during this job's download tail, when the upload
+    direction would otherwise idle; results equal sequential calls."""
     cfg = cfg or rt.ExecConfig()
     rt._check_operands(A, B, C)
     m, k = A.global_shape.rows, A.global_shape.cols
     n = B.global_shape.cols
-    if tuple(a_host.shape) != (m, k) or tuple(b_host.shape) != (k, n) or tuple(c_out.shape) != (m, n):
-        raise ContractError("host buffers must match the global shapes of A, B and C")
+    for a_host, b_host, c_out in jobs:
+        _check_host(a_host, b_host, c_out)
+        if tuple(a_host.shape) != (m, k) or tuple(b_host.shape) != (k, n) or tuple(c_out.shape) != (m, n):
+            raise ContractError("host buffers must match the global shapes of A, B and C")
     fab = A.fabric
     fab.heap.exchange()
     devs = sorted({fab.device_of(r) for r in fab.local_ranks()})
@@ -225,58 +238,112 @@ def _multiply_blocks(A, B, C, a_host, b_host, c_out, cfg, P: int, Q: int, copy_s
     results = {r: rt.RunStats() for r in fab.local_ranks()}
     rb = [m * i // P for i in range(P + 1)]
     cb = [n * j // Q for j in range(Q + 1)]
-    a_ev: dict = {}
-    b_ev: dict = {}
+    order = _shell_order(P, Q)
+    # per block of the previous job: its compute-done and download-done events;
+    # per panel: the compute-done events of the previous job's last block reading it
+    a_free: dict = {}
+    b_free: dict = {}
+    c_free: dict = {}
     done_all = []
-    for step, (i, j) in enumerate(_shell_order(P, Q)):
-        r0, r1, c0, c1 = rb[i], rb[i + 1], cb[j], cb[j + 1]
-        if r1 <= r0 or c1 <= c0:
-            continue
-        if i not in a_ev:                     # A row panel i, the first time a block needs it
-            up: dict = {}
-            _copy_rows(A, a_host, r0, r1, lambda d: h2d_s[d][0], True, up)
-            a_ev[i] = [e for evs in up.values() for e in evs]
-        if j not in b_ev:                     # B column panel j
-            up = {}
-            _copy_rows(B, b_host, 0, k, lambda d: h2d_s[d][0], True, up, c0, c1)
-            b_ev[j] = [e for evs in up.values() for e in evs]
-        ready = a_ev[i] + b_ev[j]
-        if cross:
-            fab.synchronize()
-        runs = []
-        for r in fab.local_ranks():
-            ops = [o for o in (_restrict(op, r0, r1, c0, c1) for op in full_ops[r]) if o is not None]
-            if not ops:
+    for a_host, b_host, c_out in jobs:
+        a_ev: dict = {}
+        b_ev: dict = {}
+        a_last: dict = {}
+        b_last: dict = {}
+        c_down: dict = {}
+        for step, (i, j) in enumerate(order):
+            r0, r1, c0, c1 = rb[i], rb[i + 1], cb[j], cb[j + 1]
+            if r1 <= r0 or c1 <= c0:
                 continue
-            pkey = ("block", cfg.stationarity, cfg.staging, cfg.same_device_gets, r, r0, r1, c0, c1)
-            cache = rt.schedule_cache(A, B, C)
-            sched = cache.get(pkey)
-            if sched is None:
-                sched = cache[pkey] = rt.lower_direct(A, B, C, cfg, r, ops=ops)
-            rt._count_reference_traffic(A, B, C, cfg, sched)
-            runs.append(rt._RankRun(A, B, C, cfg, sched, ready).issue())
-        done = [run.done for run in runs]
-        for run in runs:
-            st = results[run.caller]
-            st.executed_ops += run.stats.executed_ops
-            st.device_order += run.stats.device_order
-            st.a_requests += run.stats.a_requests
-            st.b_requests += run.stats.b_requests
-            st.launches += run.stats.launches
-            st.gets += run.stats.gets
-            st.staged_bytes += run.stats.staged_bytes
-        if cross:
-            fab.synchronize()
-        s_down = step % nst
-        for d in devs:
-            for ev in done:
-                d2h_s[d][s_down].wait_event(ev)
-        down: dict = {}
-        _copy_rows(C, c_out, r0, r1, lambda d: d2h_s[d][s_down], False, down, c0, c1)
-        done_all += [e for evs in down.values() for e in evs] + done
+            if i not in a_ev:                     # A row panel i, the first time a block needs it
+                for d in devs:
+                    for ev in a_free.get(i, ()):
+                        h2d_s[d][0].wait_event(ev)
+                up: dict = {}
+                _copy_rows(A, a_host, r0, r1, lambda d: h2d_s[d][0], True, up)
+                a_ev[i] = [e for evs in up.values() for e in evs]
+            if j not in b_ev:                     # B column panel j
+                for d in devs:
+                    for ev in b_free.get(j, ()):
+                        h2d_s[d][0].wait_event(ev)
+                up = {}
+                _copy_rows(B, b_host, 0, k, lambda d: h2d_s[d][0], True, up, c0, c1)
+                b_ev[j] = [e for evs in up.values() for e in evs]
+            ready = a_ev[i] + b_ev[j] + list(c_free.get((i, j), ()))
+            if cross:
+                fab.synchronize()
+            runs = []
+            for r in fab.local_ranks():
+                ops = [o for o in (_restrict(op, r0, r1, c0, c1) for op in full_ops[r]) if o is not None]
+                if not ops:
+                    continue
+                pkey = ("block", cfg.stationarity, cfg.staging, cfg.same_device_gets, r, r0, r1, c0, c1)
+                cache = rt.schedule_cache(A, B, C)
+                sched = cache.get(pkey)
+                if sched is None:
+                    sched = cache[pkey] = rt.lower_direct(A, B, C, cfg, r, ops=ops)
+                rt._count_reference_traffic(A, B, C, cfg, sched)
+                runs.append(rt._RankRun(A, B, C, cfg, sched, ready).issue())
+            done = [run.done for run in runs]
+            a_last[i] = done
+            b_last[j] = done
+            for run in runs:
+                st = results[run.caller]
+                st.executed_ops += run.stats.executed_ops
+                st.device_order += run.stats.device_order
+                st.a_requests += run.stats.a_requests
+                st.b_requests += run.stats.b_requests
+                st.launches += run.stats.launches
+                st.gets += run.stats.gets
+                st.staged_bytes += run.stats.staged_bytes
+            if cross:
+                fab.synchronize()
+            s_down = step % nst
+            for d in devs:
+                for ev in done:
+                    d2h_s[d][s_down].wait_event(ev)
+            down: dict = {}
+            _copy_rows(C, c_out, r0, r1, lambda d: d2h_s[d][s_down], False, down, c0, c1)
+            c_down[(i, j)] = [e for evs in down.values() for e in evs]
+            done_all += c_down[(i, j)] + done
+        a_free, b_free, c_free = a_last, b_last, c_down
     rt._join_current(fab, done_all)
     for r, st in results.items():
         st.flops = int(fab.counters.flops[r])
+    return results
+
+
+@nvtx("um:multiply_from_host_many")
+def multiply_from_host_many(A, B, C, jobs, cfg: rt.ExecConfig | None = None, panels: int = 4,
+                            col_panels: int | None = None) -> dict:
+    """A sequence of end-to-end multiplies, each C += a @ b with its own host
+    buffers: jobs = [(a_host, b_host, c_out), ...]; c_out of job s receives C
+    after job s, exactly as len(jobs) calls of multiply_from_host would.
+
+    Issued as one pipeline over the P x Q block grid (_multiply_blocks_jobs):
+    job s + 1's uploads start as soon as job s no longer reads the device
+    panel they overwrite, i.e. during job s's download tail, instead of after
+    job s's last download.  Every job still uploads all of its A and B and
+    downloads all of C; in steady state the step time falls from the one-job
+    pipeline floor (>= 1.25 x the PCIe floor) towards max(upload, download).
+    Unreplicated C, single process; otherwise the jobs run one call each."""
+    jobs = list(jobs)
+    if not jobs:
+        return {}
+    if col_panels is None:
+        big_b = B.global_shape.rows * B.global_shape.cols * 4 >= A.global_shape.rows * A.global_shape.cols
+        col_panels = panels if (big_b and C.c == 1) else 1
+    if col_panels > 1 and C.c == 1 and not rt._cross_process(A, B, C, cfg or rt.ExecConfig()):
+        return _multiply_blocks_jobs(A, B, C, jobs, cfg, panels, col_panels, 1)
+    results: dict = {}
+    for a_host, b_host, c_out in jobs:
+        for r, st in multiply_from_host(A, B, C, a_host, b_host, c_out, cfg, panels=panels,
+                                        col_panels=col_panels).items():
+            acc = results.setdefault(r, rt.RunStats())
+            for f in ("executed_ops", "device_order", "a_requests", "b_requests", "launches", "gets",
+                      "staged_bytes"):
+                setattr(acc, f, getattr(acc, f) + getattr(st, f))
+            acc.flops = st.flops
     return results
 
 
