@@ -112,8 +112,9 @@ def multiply_from_host(A, B, C, a_host: torch.Tensor, b_host: torch.Tensor, c_ou
     of B first leaves the download direction idle for B's whole transfer),
     else row panels (Q = 1, B uploaded whole first).  Measured at cfg5 p = 1
     on one B200 (tools/e2e_probe.py), eager issue: 32 x 1 row panels 34.3 ms
-    per step, 4 x 4 blocks 31.3, 8 x 8 33.4 (host-bound: the issue of 64
-    blocks); CapturedHostMultiply removes the host cost of fine grids.
+    per step, 4 x 4 blocks 31.3, 8 x 8 33.4 (not host-bound: the issue costs
+    0.06 ms per block; the finer grid's smaller strided copies are slower
+    than its shorter fill and drain gain, profiles/r2_s4_e2e_grid_many.log).
     """
     _check_host(a_host, b_host, c_out)
     if col_panels is None:
