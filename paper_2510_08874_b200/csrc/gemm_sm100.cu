@@ -429,7 +429,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
   // the stream (launched with programmatic stream serialization); every
   // global access comes after the wait for that kernel's completion.
   ptx::griddep_wait();
-  ptx::griddep_launch_dependents();
+  // a launch that waits on copy-engine arrivals keeps its dependents out until
+  // it exits: their CTAs, resident early, would take the SMs left free for
+  // copies the driver runs with SMs (same-device 2-D copies)
+  if (!args.ext_waits) ptx::griddep_launch_dependents();
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int s = 0; s < args.nslots; ++s)   // a slot whose ops have no tile is complete at once
       if (args.slots[s].expected == 0) ptx::red_release_sys_add_u32(args.slots[s].flag, args.slots[s].increment);
@@ -1957,7 +1960,11 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   if (works.size() <= (size_t)MAX_INLINE_OPS && !maps_global) {
     memcpy(args.inl_maps, maps.data(), maps.size() * sizeof(CUtensorMap));
     memcpy(args.inl_works, works.data(), works.size() * sizeof(Work));
-    args.smem_works = knobs().smem_works && works.size() <= (size_t)SMEM_WORKS ? 1 : 0;
+    // (launches waiting on copy-engine arrival flags keep the parameter-block
+    // list: with the shared-memory copy they hung under compute-sanitizer
+    // racecheck, which serialises the device; plain, memcheck and synccheck
+    // runs pass either way -- profiles/r2_sanitizer.md, session 4)
+    args.smem_works = knobs().smem_works && works.size() <= (size_t)SMEM_WORKS && !args.ext_waits ? 1 : 0;
   } else {
     // large op lists: one stream-ordered allocation carries work list + tensor maps
     args.smem_works = 0;
