@@ -327,14 +327,16 @@ def multiply_from_host_many(A, B, C, jobs, cfg: rt.ExecConfig | None = None, pan
     job s's last download.  Every job still uploads all of its A and B and
     downloads all of C; in steady state the step time falls from the one-job
     pipeline floor (>= 1.25 x the PCIe floor) towards max(upload, download).
-    Unreplicated C, single process; otherwise the jobs run one call each."""
+    Unreplicated C, single process (row panels or blocks); otherwise the jobs
+    run one call each."""
     jobs = list(jobs)
     if not jobs:
         return {}
     if col_panels is None:
         big_b = B.global_shape.rows * B.global_shape.cols * 4 >= A.global_shape.rows * A.global_shape.cols
         col_panels = panels if (big_b and C.c == 1) else 1
-    if col_panels > 1 and C.c == 1 and not rt._cross_process(A, B, C, cfg or rt.ExecConfig()):
+    if C.c == 1 and not rt._cross_process(A, B, C, cfg or rt.ExecConfig()):
+        # (col_panels == 1: row panels of C, all of B as the one column panel)
         return _multiply_blocks_jobs(A, B, C, jobs, cfg, panels, col_panels, 1)
     results: dict = {}
     for a_host, b_host, c_out in jobs:
