@@ -560,10 +560,13 @@ def e2e_run(args, A, B, C, cfg, flops, dev, barrier, max_over_ranks):
         api = ("hostio.multiply_from_host" if (world > 1 or not args.e2e_graph)
                else "hostio.CapturedHostMultiply (multiply_from_host as one CUDA graph)")
     # the e2e roofline: this box's pinned-memory copy bandwidth, each direction
-    # alone and both at once (PCIe is full duplex); floor = the slower direction
-    # of the concurrent pair
+    # alone and both at once (PCIe is full duplex); floor = the smaller volume
+    # moved in both directions at once at the concurrent rate, then the rest
+    # of the larger one alone
     bw = pcie_bandwidth(dev)
-    floor_ms = max(h2d / bw["h2d_concurrent_gbs"], d2h / bw["d2h_concurrent_gbs"]) / 1e6
+    both = min(h2d, d2h)
+    rest_ms = (h2d - both) / bw["h2d_gbs"] / 1e6 + (d2h - both) / bw["d2h_gbs"] / 1e6
+    floor_ms = max(both / bw["h2d_concurrent_gbs"], both / bw["d2h_concurrent_gbs"]) / 1e6 + rest_ms
     # the same copies in the order multiply_from_host issues them, each C block
     # downloadable only once its A rows and B columns are up (and computed at
     # the measured peak): the floor of this block pipeline, not only of PCIe
