@@ -84,6 +84,13 @@ class ExecConfig:
                          replicas on distinct multicast-capable GPUs), "nccl"
                          (ncclReduce per tile; barrier form), "auto" (nvls when
                          capable, else peer).
+      graph_replay       a small single-process direct multiply (<= 2^36 flops)
+                         repeated on the same (A, B, C, config) is captured into
+                         a CUDA graph on its third call and replayed from then
+                         on (graphs.CapturedMultiply): one cudaGraphLaunch
+                         instead of the per-rank host issue that dominates such
+                         multiplies.  Same kernels and plans; a replicated C is
+                         reduced in the barrier form inside the graph.
     """
 
     stationarity: Stationarity = Stationarity.STATIONARY_C
@@ -106,6 +113,7 @@ class ExecConfig:
     reduce_panels: int = 4
     k_split: int = 0
     reduce_mode: str = "auto"
+    graph_replay: bool = True
 
     def __post_init__(self):
         if self.prefetch_depth < 1 or self.max_inflight_gemms < 1 or self.max_inflight_accums < 1:

@@ -30,7 +30,9 @@ return, so torch code sees the results without host synchronisation.
 
 from __future__ import annotations
 
+import copy
 import ctypes
+import dataclasses
 
 import torch
 
@@ -300,6 +302,50 @@ def _share_sms(fab, ranks) -> dict:
     return caps
 
 
+GRAPH_MAX_FLOPS = 1 << 36   # graph_replay: multiplies up to ~42 us of tensor-core time
+GRAPH_AFTER = 2             # eager multiplies of one (A, B, C, config) before it is captured
+
+
+def _graph_replay(A, B, C, cfg: ExecConfig) -> dict[int, RunStats] | None:
+    """ExecConfig.graph_replay: the third and later calls of a small direct
+    multiply on the same (A, B, C, config) run as one CUDA graph replay.
+
+    The host issue of a multiply (per rank: plan lookup, stream fork/join, a
+    ctypes call per launch) costs ~50 us, more than the GPU work of a 1024^3
+    multiply.  Eligible: one process, every local rank on the current device,
+    <= GRAPH_MAX_FLOPS, not inside another capture, launch tracing off.  The
+    graph lives in A's schedule cache next to the plans it replays (dropped
+    with them).  Returns None when the caller must run the multiply eagerly."""
+    fab = A.fabric
+    m, k = A.global_shape.rows, A.global_shape.cols
+    n = B.global_shape.cols
+    if (2 * m * n * k > GRAPH_MAX_FLOPS or fab.world.size != 1 or engine.TRACE_ENABLED
+            or torch.cuda.is_current_stream_capturing()):
+        return None
+    dev = torch.cuda.current_device()
+    if any(fab.device_of(r) != dev for r in fab.local_ranks()):
+        return None
+    cache = schedule_cache(A, B, C)
+    key = ("graph", tuple(cfg.__dict__.values()), dev)     # field values: enums, ints, strings
+    hit = cache.get(key, 0)
+    if isinstance(hit, int):
+        if hit < GRAPH_AFTER:
+            cache[key] = hit + 1
+            return None
+        from paper_2510_08874_b200.graphs import CapturedMultiply
+
+        # runs this call's multiply eagerly (warmup=1), then captures the next
+        cache[key] = CapturedMultiply(A, B, C, dataclasses.replace(cfg, graph_replay=False), warmup=1)
+        stats = cache[key].stats
+    else:
+        stats = hit.replay()
+    out = {}
+    for r, st in stats.items():
+        out[r] = copy.copy(st)
+        out[r].flops = int(fab.counters.flops[r])     # as the eager path reports it
+    return out
+
+
 @nvtx("um:execute_multiply")
 def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedMatrix, cfg: ExecConfig,
                      execution: str = "direct", machine=None, max_compute: int | None = None,
@@ -313,6 +359,10 @@ def execute_multiply(A: DistributedMatrix, B: DistributedMatrix, C: DistributedM
     if execution not in ("direct", "ir:greedy", "ir:cost", "ir:exhaustive"):
         raise ValueError(f"unknown execution mode {execution!r}")
     _check_operands(A, B, C)
+    if execution == "direct" and cfg.graph_replay:
+        replayed = _graph_replay(A, B, C, cfg)
+        if replayed is not None:
+            return replayed
     fab = A.fabric
     fab.heap.exchange()
     ranks = fab.local_ranks()
