@@ -44,8 +44,9 @@ class CapturedMultiply:
         self.A, self.B, self.C, self.cfg = A, B, C, cfg
         # eager runs build the schedules, issue plans, staging pools and per-stream
         # scheduler counters, so nothing is allocated while capturing (they are
-        # real multiplies: C += A @ B each, counted like any other)
-        for _ in range(max(1, warmup)):
+        # real multiplies: C += A @ B each, counted like any other).  warmup=0
+        # only when the caller has just run this very multiply (same config).
+        for _ in range(max(0, warmup)):
             rt.execute_multiply(A, B, C, cfg, **run)
         torch.cuda.synchronize()
         before = fab.counters.__class__(fab.counters.nprocs)

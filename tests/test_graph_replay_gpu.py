@@ -89,3 +89,25 @@ def test_graph_replay_skipped_while_tracing_and_per_config(cuda):
     assert len(_graphs(A, B, C)) == 2
     torch.cuda.synchronize()
     assert np.array_equal(C.gather(0), 10 * (a @ b))
+
+
+def test_failed_capture_stays_eager(cuda, monkeypatch):
+    """A multiply whose capture fails keeps running eagerly, exactly, with
+    counters of one multiply per call (the failed capture's host-side
+    counting is rolled back)."""
+    fab, A, B, C, a, b = build_problem(384, 320, 512, 4, "2d", "col", "2d", 1, 1, 2, seed=53)
+
+    def boom(self, A_, *args, **kwargs):
+        A_.fabric.counters.add_traffic(0, 1, 12345)        # host-side counting ran, then the capture failed
+        raise RuntimeError("capture refused")
+
+    monkeypatch.setattr(CapturedMultiply, "__init__", boom)
+    execute_multiply(A, B, C, ExecConfig())
+    torch.cuda.synchronize()
+    bytes1 = fab.counters.bytes.copy()
+    for _ in range(4):
+        C.zero_()
+        execute_multiply(A, B, C, ExecConfig())
+        assert np.array_equal(C.gather(0), a @ b)
+    assert not _graphs(A, B, C)
+    assert np.array_equal(fab.counters.bytes, 5 * bytes1)
