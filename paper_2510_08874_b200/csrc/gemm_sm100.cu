@@ -278,7 +278,11 @@ constexpr int PS_OFF = TL_CHUNK_OFF + TL_CHUNKS;        // per CTA: producer cyc
                                                       // stage, load latency sum (issue -> full), count, max
 constexpr int PS_WORDS = 8;
 constexpr int PROF_WORDS = PS_OFF + 160 * PS_WORDS;
-constexpr int CHUNK_FLAGS_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
+// per-stream counter words: [0] next tile, [1] finished pairs, [2] next get chunk,
+// [3, 3 + MAX_GETS) chunks landed per get, then completion-slot tallies, the
+// CTA exit count, and the per-chunk landed flags
+constexpr int EXIT_OFF = 3 + UM_GEMM_MAX_GETS + UM_GEMM_MAX_SIGNALS;
+constexpr int CHUNK_FLAGS_OFF = EXIT_OFF + 1;
 
 // Completion signal: once every tile of every op naming this slot has been
 // written (all epilogue warps of both CTAs of each tile arrive), the kernel
@@ -1169,6 +1173,29 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
     ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
     if (lane == 0) stamp(10);
   }
+  // Every warp of this CTA is done with the stream's get / completion-slot
+  // counters and chunk flags: the last CTA out re-zeroes what this launch
+  // used, so the next launch on the stream (stream order, or griddepcontrol.wait
+  // under programmatic launch) finds them zero without a host memset.
+  if (args.ngets > 0 || args.nslots > 0) {
+    int* const ctr = args.counters;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      tq[0] = atomicAdd(&ctr[EXIT_OFF], 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (tq[0]) {
+      __threadfence();
+      const int nflags = min(args.total_chunks, MAX_CHUNK_FLAGS);
+      for (int i = threadIdx.x; i < nflags; i += blockDim.x) ctr[CHUNK_FLAGS_OFF + i] = 0;
+      for (int i = threadIdx.x; i < args.ngets; i += blockDim.x) ctr[3 + i] = 0;
+      for (int i = threadIdx.x; i < args.nslots; i += blockDim.x) ctr[3 + MAX_GETS + i] = 0;
+      if (threadIdx.x == 0) {
+        ctr[2] = 0;
+        ctr[EXIT_OFF] = 0;
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -1289,9 +1316,10 @@ static const Knobs& knobs() {
   return k;
 }
 
-// Per-(device, stream) scheduler counters {next tile, finished clusters}:
-// zeroed once at creation, re-zeroed by the last cluster of every launch, so
-// launches on one stream (serialised) reuse them with no per-launch memset.
+// Per-(device, stream) scheduler counters (layout at EXIT_OFF): zeroed once at
+// creation; the tile words are re-zeroed by the last pair to leave the tile
+// scheduler and the get / slot words and chunk flags by the last CTA to exit,
+// so launches on one stream (serialised) reuse them with no per-launch memset.
 static int* stream_counters(int device, cudaStream_t stream) {
   static std::mutex mu;
   static std::vector<std::pair<std::pair<int, cudaStream_t>, int*>> table;
@@ -1994,15 +2022,9 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
   for (const StageCopy& c : P->copies)
     UM_CUDA_CHECK(cudaMemcpy2DAsync(c.dst, c.dpitch, c.src, c.spitch, c.width, c.height, cudaMemcpyDefault, stream));
   LaunchArgs& args = P->args;
+  // zero at creation and re-zeroed by the last CTA of every launch (kernel exit)
   args.counters = stream_counters(P->device, stream);
   if (!args.counters) return fail(UM_ECUDA, "could not allocate the scheduler counters");
-  if (P->ngets) {
-    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 2, 0, (1 + P->ngets) * sizeof(int), stream));
-    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + CHUNK_FLAGS_OFF, 0,
-                                  std::min(args.total_chunks, MAX_CHUNK_FLAGS) * sizeof(int), stream));
-  }
-  if (P->nslots)
-    UM_CUDA_CHECK(cudaMemsetAsync(args.counters + 3 + MAX_GETS, 0, P->nslots * sizeof(int), stream));
   // profiling (UM_GEMM_STALLS=1): MMA-thread stall breakdown, synchronous, printed to stderr
   static const bool stalls = env_int("UM_GEMM_STALLS", 0) != 0;
   unsigned long long* prof = nullptr;

@@ -16,7 +16,7 @@ p = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 m, n, k, ap, bp, cp, fa, fb, fc, desc = bench.CONFIGS[name]
 fab, A, B, C, _, _ = build_problem(m, n, k, p, ap, bp, cp, fa(p), fb(p), fc(p), seed=0, real=True, synthetic=True,
                                    devices=[0])
-cfg = ExecConfig()
+cfg = ExecConfig(graph_replay=os.environ.get("UM_GRAPH_REPLAY", "0") == "1")   # eager issue by default
 for _ in range(10):
     execute_multiply(A, B, C, cfg)
 torch.cuda.synchronize()
@@ -26,4 +26,5 @@ for _ in range(300):
     execute_multiply(A, B, C, cfg)
 pr.disable()
 torch.cuda.synchronize()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
