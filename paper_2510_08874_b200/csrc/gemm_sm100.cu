@@ -162,8 +162,7 @@ struct alignas(16) GetDesc {
   int32_t rows, row_bytes;
   int32_t rows_per_chunk, nchunks;
   int32_t chunk_start, vec;       // vec: 16-byte aligned rows (vector path)
-  int32_t row0;                   // first row of the band in its staging buffer (fine-grained waits)
-  int32_t ilv;                    // 1: pulled interleaved with the next get in pull order (see the get engine)
+  int32_t row0, pad_;             // first row of the band in its staging buffer (fine-grained waits)
 };
 
 // the work whose tile range holds tile t: the last work with tile_start <= t
@@ -1083,27 +1082,9 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
       }
       int oi = 0;
       while (oi + 1 < args.ngets && args.gets[args.get_order[oi + 1]].chunk_start <= c) ++oi;
-      // a pair of gets first needed together (an op's A band and B band) is
-      // pulled interleaved, in proportion to their sizes, over their joint
-      // chunk range, so the op's first tiles find rows of both early; chunk
-      // flags and counts stay indexed by each get's own chunk numbers
-      int lc = c;   // chunk number in the get's own range (chunk_start + local)
-      if (oi > 0 && args.gets[args.get_order[oi - 1]].ilv) --oi;
-      if (args.gets[args.get_order[oi]].ilv) {
-        const GetDesc& g1 = args.gets[args.get_order[oi]];
-        const long n1 = g1.nchunks, nn = n1 + args.gets[args.get_order[oi + 1]].nchunks;
-        const long i = c - g1.chunk_start;
-        const long f0 = (i * n1) / nn, f1 = ((i + 1) * n1) / nn;
-        if (f1 > f0) {
-          lc = g1.chunk_start + (int)f0;
-        } else {
-          ++oi;
-          lc = args.gets[args.get_order[oi]].chunk_start + (int)(i - f0);
-        }
-      }
       const int j = args.get_order[oi];
       const GetDesc& g = args.gets[j];
-      const int r0 = (lc - g.chunk_start) * g.rows_per_chunk;
+      const int r0 = (c - g.chunk_start) * g.rows_per_chunk;
       const int r1 = min(g.rows, r0 + g.rows_per_chunk);
       constexpr int U = 16;  // 16-byte loads in flight per lane (4 warps: 32 KiB per SM)
       if (g.vec == 2) {
@@ -1179,7 +1160,7 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
 #if UM_PROFILE
         if (args.prof && c < TL_CHUNKS) args.prof[TL_CHUNK_OFF + c] = ptx::globaltimer();
 #endif
-        if (lc < MAX_CHUNK_FLAGS) ptx::st_release_gpu_s32(&args.counters[CHUNK_FLAGS_OFF + lc], 1);
+        if (c < MAX_CHUNK_FLAGS) ptx::st_release_gpu_s32(&args.counters[CHUNK_FLAGS_OFF + c], 1);
       }
     }
   }
@@ -1287,7 +1268,6 @@ struct Knobs {
   int chain_waves = 6;
   int pdl = 1;
   int pull_order = 1;
-  int pull_pairs = 1;
   int tail_split = 0;
   int cpf = 0;
   int stagger = 0;
@@ -1326,7 +1306,6 @@ static const Knobs& knobs() {
     k.chain_waves = env_int("UM_GEMM_CHAIN_WAVES", 6);
     k.pdl = env_int("UM_GEMM_PDL", 1) ? 1 : 0;
     k.pull_order = env_int("UM_GEMM_PULL_ORDER", 1) ? 1 : 0;
-    k.pull_pairs = env_int("UM_GEMM_PULL_PAIRS", 1) ? 1 : 0;
     k.tail_split = env_int("UM_GEMM_TAIL_SPLIT", 0);
     k.cpf = std::max(0, env_int("UM_GEMM_CPF", 0));
     k.stagger = std::max(0, env_int("UM_GEMM_STAGGER", 0));
@@ -1913,9 +1892,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   // segments of later first-wave tiles (UM_GEMM_PULL_ORDER=0 keeps it).
   std::vector<int> gorder(std::max(0, ngets));
   for (int i = 0; i < ngets; ++i) gorder[i] = i;
-  std::vector<double> need_time(std::max(ngets, 0), 1e300);
   if (ngets > 1 && kn.pull_order) {
-    std::vector<double>& need_t = need_time;
+    std::vector<double> need_t(ngets, 1e300);
     int pairs = 148;
     cudaDeviceGetAttribute(&pairs, cudaDevAttrMultiProcessorCount, device);
     pairs = std::max(1, pairs / CG);
@@ -1980,22 +1958,8 @@ static int prepare(const um_gemm_op* ops_in, int nops, const um_get_desc* gets_i
   for (int oi = 0; oi < ngets; ++oi) {   // chunk ranges in pull order
     GetDesc& g = args.gets[gorder[oi]];
     g.chunk_start = chunks;
-    g.ilv = 0;
     chunks += g.nchunks;
   }
-  // gets the list schedule first needs at the same moment (ties in pull order,
-  // e.g. the A band and the B band of the launch's first op) are pulled in
-  // interleaved pairs
-  if (ngets > 1 && kn.pull_order && kn.pull_pairs)
-    for (int oi = 0; oi + 1 < ngets; ++oi) {
-      GetDesc& a = args.gets[gorder[oi]];
-      const GetDesc& b = args.gets[gorder[oi + 1]];
-      if (need_time[gorder[oi]] < 1e299 && need_time[gorder[oi]] == need_time[gorder[oi + 1]] && a.nchunks > 0 &&
-          b.nchunks > 0) {
-        a.ilv = 1;
-        ++oi;
-      }
-    }
   args.ngets = ngets;
   args.total_chunks = chunks;
   if (chunks > MAX_CHUNK_FLAGS)   // too many chunks for per-chunk flags: whole-band waits instead

@@ -73,7 +73,6 @@ PROF_ONLY = ("UM_GEMM_PAIRS", "UM_GEMM_EPI_WARPS", "UM_GEMM_CG", "UM_GEMM_EPI_DE
     {"UM_GEMM_EPI_DEBUG": "red"},                        # red.global epilogue for local C
     {"UM_GEMM_APOL": "0", "UM_GEMM_BPOL": "0", "UM_GEMM_CPOL": "1"},
     {"UM_GEMM_TAIL_SPLIT": "1"},                         # last wave split along k (fused launches, gets)
-    {"UM_GEMM_PULL_PAIRS": "0"},                         # pulls needed together not interleaved
     {"UM_GEMM_SKSTART": "0"},                            # no staggered start
     {"UM_GEMM_CG": "1"},                                 # cta_group::1 (profiling build)
     {"UM_GEMM_PDL": "0"},                                # without programmatic dependent launch
