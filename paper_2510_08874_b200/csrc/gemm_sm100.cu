@@ -255,6 +255,10 @@ constexpr int MAX_GETS = UM_GEMM_MAX_GETS;
 constexpr int GET_CHUNK_BYTES = 32 * 1024;
 constexpr int MAX_SLOTS = UM_GEMM_MAX_SIGNALS;
 constexpr int MAX_CHUNK_FLAGS = 1 << 16;  // per-chunk landed flags (fine-grained waits)
+#ifndef UM_B_WAIT_KB
+#define UM_B_WAIT_KB 8
+#endif
+constexpr int B_WAIT_KB = UM_B_WAIT_KB;   // k-blocks of B rows waited for at once (fine waits)
 // UM_PROFILE=1 (the separate libunimul_b200_prof.so, `make prof`) compiles in
 // the MMA-thread wait accounting and the block-0 timeline behind UM_GEMM_STALLS.
 // The default library has none of it: even untaken checks in the MMA issuer's
@@ -277,7 +281,11 @@ constexpr int TL_CHUNK_OFF = TL_OFF + 128 * TL_TILES * 3;
 constexpr int PS_OFF = TL_CHUNK_OFF + TL_CHUNKS;        // per CTA: producer cycles, producer waits for a free
                                                       // stage, load latency sum (issue -> full), count, max
 constexpr int PS_WORDS = 8;
-constexpr int PROF_WORDS = PS_OFF + 160 * PS_WORDS;
+// (profiling) CTAs 0 and 1: per k-block of their first unit, when the producer
+// issued the loads (after its stage and operand waits), and when its A rows landed
+constexpr int KB_OFF = PS_OFF + 160 * PS_WORDS;
+constexpr int KB_MAX = 512;
+constexpr int PROF_WORDS = KB_OFF + 2 * (KB_MAX + 1);
 // per-stream counter words: [0] next tile, [1] finished pairs, [2] next get chunk,
 // [3, 3 + MAX_GETS) chunks landed per get, then completion-slot tallies, the
 // CTA exit count, and the per-chunk landed flags
@@ -607,6 +615,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
         const int arow = wk.a_row0 + mb * BM * CG * NP + row_off;
         const int bcol = wk.b_col0 + nb * NT + (int)cta_rank * (C::UN / CG);
         if (a_fine && lane == 0) wait_rows(a_fine - 1, arow, arow + BM);   // this CTA's A rows, all k
+#if UM_PROFILE
+        if (args.prof && i == 0 && w == w0 && blockIdx.x < 2 && lane == 0)
+          args.prof[KB_OFF + blockIdx.x * (KB_MAX + 1) + KB_MAX] = ptx::globaltimer();
+#endif
         __syncwarp();
         // optional L2 prefetch `pf` k-blocks ahead of the loads (UM_GEMM_PF; off by
         // default: measured slower, 1437 -> 1143..1292 TFLOP/s on cfg2)
@@ -655,8 +667,11 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
           const uint32_t sb = ptx::smem_u32(smem_b + stage * C::B_BYTES);
           const int kcol = a_col0 + kb * BK;
           const int krow = b_row0 + kb * BK;
-          if (b_fine) {   // this k-block's B rows
-            if (lane == 0) wait_rows(b_fine - 1, krow, krow + BK);
+          if (b_fine && ((kb - kbs) % B_WAIT_KB) == 0) {
+            // the B rows of the next B_WAIT_KB k-blocks: one flag poll + acquire
+            // fence per batch (per k-block, the fences and polls of a band still
+            // landing cost ~1.7 us per k-block: 2.4 instead of 0.7 us)
+            if (lane == 0) wait_rows(b_fine - 1, krow, b_row0 + min(kb + B_WAIT_KB, kbe) * BK);
             __syncwarp();
           }
           if (kbg++ == cpf_at && issuer) {
@@ -700,6 +715,10 @@ __global__ void __launch_bounds__(num_threads(EW, GW), 1)
               }
           }
           if (i == 0 && kb == 0 && lane == 0) stamp(3);
+#if UM_PROFILE
+          if (args.prof && i == 0 && blockIdx.x < 2 && lane == 0 && kb - kbs < KB_MAX)
+            args.prof[KB_OFF + blockIdx.x * (KB_MAX + 1) + (kb - kbs)] = ptx::globaltimer();
+#endif
 #if UM_PROFILE
           {
             const unsigned long long p_now = clock64();
@@ -2088,6 +2107,13 @@ static int launch_prepared(Prepared* P, cudaStream_t stream) {
           if (h[TL_CHUNK_OFF + c])
             fprintf(f, "%d,chunk,-1,%d,%d,%llu,%llu\n", launch_no, c, c, h[TL_CHUNK_OFF + c] - t0,
                     h[TL_CHUNK_OFF + c] - t0);
+        // CTA b's first unit: loads issued for k-block kb (index kb), A rows landed (index -1)
+        for (int b = 0; b < 2; ++b)
+          for (int kb = 0; kb <= KB_MAX; ++kb) {
+            const unsigned long long v = h[KB_OFF + b * (KB_MAX + 1) + kb];
+            if (v && v >= t0)
+              fprintf(f, "%d,kb,%d,%d,%d,%llu,%llu\n", launch_no, b, kb == KB_MAX ? -1 : kb, b, v - t0, v - t0);
+          }
         fclose(f);
       }
       ++launch_no;

@@ -28,10 +28,10 @@ for _ in range(3):
     run_direct(A, B, C, cfg, rank)
 torch.cuda.synchronize()
 path = os.environ["UM_GEMM_TIMELINE"]
-tiles, chunks = defaultdict(list), defaultdict(list)
+tiles, chunks, kbs = defaultdict(list), defaultdict(list), defaultdict(list)
 with open(path) as f:
     for r in csv.DictReader(f):
-        (tiles if r["kind"] == "tile" else chunks)[int(r["launch"])].append(r)
+        {"tile": tiles, "chunk": chunks, "kb": kbs}[r["kind"]][int(r["launch"])].append(r)
 L = max(tiles)
 ts = [(int(r["pair"]), int(r["start_ns"]), int(r["end_ns"])) for r in tiles[L]]
 ch = sorted(int(r["start_ns"]) for r in chunks[L])
@@ -48,3 +48,12 @@ for b0 in range(0, span, B_NS):
     med = statistics.median(started) if started else 0.0
     print(f"  {b0 / 1e3:6.0f}-{b1 / 1e3:4.0f} us: pairs busy {busy:4.0%}, tiles started {len(started):3d} "
           f"(median span {med:6.1f} us), chunks landed {landed}")
+
+# profiling build: CTAs 0 / 1, first unit: A rows landed, loads issued per k-block
+for cta in (0, 1):
+    rec = {int(r["index"]): int(r["start_ns"]) / 1e3 for r in kbs[L] if int(r["pair"]) == cta}
+    if rec:
+        ks = sorted(k for k in rec if k >= 0)
+        marks = [k for k in ks if k in (0, 1, 2, 4, 8, 16, 32, 48, 64, 80, 96, 112) or k == ks[-1]]
+        print(f"  CTA {cta} first unit: A rows landed {rec.get(-1, float('nan')):.1f} us; loads issued at kb "
+              + ", ".join(f"{k}: {rec[k]:.1f}" for k in marks) + " us")
